@@ -1,0 +1,176 @@
+/*
+ * ivftq_b200.h -- C ABI of the B200-native IVF-TQ search + ingest hot path.
+ *
+ * The reference (`ivftq`, pure Python/numpy, /root/reference/pkg/src/ivftq)
+ * has no FFI; its boundary is the Python `IvfTqIndex` API (index.py:162-500).
+ * Every entry point below replaces one numpy stage of that path and is what
+ * a host binding (ctypes here) calls. Conventions:
+ *
+ *   - all array pointers are DEVICE pointers unless the name says `host`;
+ *   - the library never allocates or frees caller memory: scratch is passed
+ *     in, sized by the matching *_scratch_bytes query;
+ *   - every launch is asynchronous on the caller's `stream` (cudaStream_t
+ *     passed as void*, NULL = legacy default stream);
+ *   - return value 0 = success, < 0 = an IVFTQ_ERR_* code; the message is in
+ *     ivftq_last_error() (thread-local);
+ *   - no global mutable state: concurrent calls on different streams are safe.
+ */
+#ifndef IVFTQ_B200_H
+#define IVFTQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IVFTQ_ABI_VERSION 1
+
+#define IVFTQ_OK 0
+#define IVFTQ_ERR_ARG (-1)
+#define IVFTQ_ERR_CUDA (-2)
+#define IVFTQ_ERR_SCRATCH (-3)
+#define IVFTQ_ERR_UNSUPPORTED (-4)
+
+#define IVFTQ_F32 0
+#define IVFTQ_F64 1
+
+/* Device-resident inverted lists (replaces CoarsePartition.lists +
+ * IvfTqIndex._bins/_signs/_norms, index.py:177-185, partition.py:34).
+ * List l owns slots [list_offset[l], list_offset[l] + list_cap[l]); offsets and
+ * capacities are multiples of 128 slots. Codes of 32 consecutive slots form a
+ * block: word w of slot s is codes[((s/32)*words_per_vec + w)*32 + s%32].
+ * Each word packs `fields_per_word` coordinates of field_bits = bits+use_sign
+ * bits (field value bin*2+sign, or bin), coordinate j of the word at bit
+ * field_bits*j. Slot order inside a list is arbitrary: every result is
+ * ordered by (score desc, internal id asc), never by slot. */
+typedef struct ivftq_store {
+  int32_t dim;
+  int32_t bits;
+  int32_t use_sign;
+  int32_t n_lists;
+  int32_t field_bits;
+  int32_t fields_per_word;
+  int32_t words_per_vec;
+  int32_t max_list_size; /* host-maintained upper bound of list_size[] */
+  const int64_t* list_offset; /* [n_lists] */
+  const int32_t* list_size;   /* [n_lists] */
+  uint32_t* codes;            /* [capacity/32][words_per_vec][32] */
+  uint16_t* norms;            /* [capacity] binary16 residual norms */
+  int32_t* ids;               /* [capacity] internal id, -1 = empty slot */
+  int64_t capacity;           /* slots */
+} ivftq_store;
+
+/* ---- host-only utilities (no GPU needed) -------------------------------- */
+const char* ivftq_last_error(void);
+int ivftq_abi_version(void);
+/* Number of kernels this library has launched in the process (bench evidence). */
+unsigned long long ivftq_launch_count(void);
+/* Code layout for (dim, bits, use_sign). */
+int ivftq_code_layout(int dim, int bits, int use_sign, int* field_bits,
+                      int* fields_per_word, int* words_per_vec);
+/* float64 -> binary16 bits, round-to-nearest-even, the rule of
+ * `rnorm.astype(np.float16)` (index.py:255). Host memory. */
+int ivftq_host_double_to_half(const double* host_x, int64_t n, uint16_t* host_out);
+/* Pairwise sum-of-squares row norms, numpy's np.linalg.norm(axis=1) order
+ * (index.py:241). Host memory; used to pin the device routine on the CPU. */
+int ivftq_host_row_norms(const double* host_x, int64_t n, int dim, double* host_out);
+
+/* ---- ingest: IvfTqIndex._encode_batch (index.py:231-267) ---------------- */
+/* x (n, dim) f32 or f64 -> xn = x/||x|| f64 (index.py:238-245).
+ * *bad_row (device) receives the first row with ||x|| < 1e-12, or n. */
+int ivftq_normalize_rows(const void* x, int x_dtype, int64_t n, int dim,
+                         double* xn, int64_t* bad_row, void* stream);
+/* C = A . B^T, A (M,K) f64 row-major, B (N,K) f32/f64 row-major, C (M,N)
+ * f64/f32: coarse scores (index.py:436), rotations (rotation.py:40). */
+int ivftq_gemm_nt(const double* A, const void* B, int b_dtype, int64_t M, int N,
+                  int K, void* C, int c_dtype, void* stream);
+/* Max-IP list per row, ties -> lowest list (partition.py:45-55). */
+int ivftq_assign(const double* xn, const float* centroids, int64_t n, int n_lists,
+                 int dim, int32_t* list_out, void* stream);
+/* Residual r = xn - c_l (or xn when flat), ||r|| -> binary16 (index.py:247-255). */
+int ivftq_residuals(const double* xn, const float* centroids, const int32_t* list_ids,
+                    int64_t n, int dim, int flat, double* resid_out,
+                    uint16_t* norm_out, void* stream);
+/* unit = rot/||rot||, Lloyd-Max bin + half-bin sign (lloydmax.py:129-144),
+ * packed into words_per_vec words per row; rows whose binary16 norm is 0
+ * get all-zero codes (index.py:257-262). */
+int ivftq_quantize_pack(const double* rot, const uint16_t* norms, int64_t n, int dim,
+                        int bits, int use_sign, const double* boundaries,
+                        const double* qcent, uint32_t* words_out, void* stream);
+/* Whole encoder: normalize -> assign -> residual -> rotate -> quantize/pack.
+ * scratch >= ivftq_encode_scratch_bytes(n, dim). Outputs per row: xn (f64, for
+ * the raw store; may alias nothing), list id, binary16 norm, code words. */
+size_t ivftq_encode_scratch_bytes(int64_t n, int dim);
+int ivftq_encode(const void* x, int x_dtype, int64_t n, int dim, int bits, int use_sign,
+                 int flat, const float* centroids, int n_lists, const double* R,
+                 const double* boundaries, const double* qcent, double* xn_out,
+                 int64_t* bad_row, int32_t* list_out, uint16_t* norm_out,
+                 uint32_t* words_out, void* scratch, size_t scratch_bytes,
+                 void* stream);
+/* Re-pack per-vector unpacked bins/signs (n, dim) u8 into code words
+ * (storage load path, storage.py:152-158). */
+int ivftq_pack_codes(const uint8_t* bins, const uint8_t* signs, int64_t n, int dim,
+                     int bits, int use_sign, uint32_t* words_out, void* stream);
+
+/* ---- list store (index.py:300-308 per-row list append) ------------------ */
+int ivftq_histogram(const int32_t* list_ids, int64_t n, int n_lists, int32_t* counts,
+                    void* stream);
+/* Append n encoded rows with internal ids first_id.. into their lists.
+ * cursor: [n_lists] int32 zeroed by the call. slot_of: [>= first_id+n]. */
+int ivftq_append(const ivftq_store* store, const uint32_t* words, const uint16_t* norms,
+                 const int32_t* list_ids, int64_t n, int64_t first_id,
+                 int32_t* cursor, int64_t* slot_of, void* stream);
+/* Move every list from src's segments to dst's (capacity growth). */
+int ivftq_relayout(const ivftq_store* src, const ivftq_store* dst, int64_t* slot_of,
+                   void* stream);
+/* Unpack rows [first, first+n) by internal id to (n, dim) bins / signs u8
+ * (the `bins`/`signs` views, index.py:319-325). signs may be NULL. */
+int ivftq_export_codes(const ivftq_store* store, const int64_t* slot_of, int64_t first,
+                       int64_t n, uint8_t* bins, uint8_t* signs, void* stream);
+/* Apply XOR masks to stored codes in place, by internal id (bit_flip_ablation,
+ * index.py:578-594): mask (n, dim) u8 of field bits to flip. */
+int ivftq_xor_codes(const ivftq_store* store, const int64_t* slot_of, int64_t n,
+                    const uint8_t* mask, int which /*0 bins,1 signs*/, int flip,
+                    void* stream);
+
+/* ---- search: IvfTqIndex.search_batch (index.py:409-483) ------------------ */
+/* Per row of `scores` (rows, cols) f64: the n largest by (value desc, col asc)
+ * -> idx_out/val_out (rows, n), the stable argsort probe order (index.py:438). */
+int ivftq_select_topn(const double* scores, int64_t rows, int cols, int n,
+                      int32_t* idx_out, double* val_out, void* stream);
+/* Coarse probes: scores qn.C^T in f64 then select (index.py:436-438). */
+size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists);
+int ivftq_probe(const double* qn, const float* centroids, int64_t nq, int n_lists,
+                int dim, int n_p, int32_t* probe_out, double* coarse_out,
+                void* scratch, size_t scratch_bytes, void* stream);
+/* List scan + per-query top-`depth` (index.py:441-483): score =
+ * coarse + (double)(||r|| * sum_j qrot_j * levels[code_j]). levels: f64
+ * flattened reconstruction table (lloydmax.py:146-150). ids are internal. */
+size_t ivftq_scan_scratch_bytes(int64_t nq, int n_p, int depth);
+int ivftq_scan_topk(const ivftq_store* store, const int32_t* probe, const double* coarse,
+                    const float* qrot, const double* levels, int64_t nq, int n_p,
+                    int depth, int64_t* ids_out, double* scores_out, void* scratch,
+                    size_t scratch_bytes, void* stream);
+/* Exact re-score of the top-depth candidates against the raw f32 store and
+ * re-order to top-k (index.py:470-473). */
+int ivftq_rerank(const float* raw, const double* qn, const int64_t* cand_ids,
+                 int64_t nq, int depth, int dim, int k, int64_t* ids_out,
+                 double* scores_out, void* stream);
+/* Decode rows by internal id: c_l + ||r|| R^T T[code], optionally renormalised
+ * (refresh.reconstruct_all, refresh.py:63-81). R_T is the TRANSPOSED rotation
+ * (row-major R^T), so the device GEMM computes T[code] . R. */
+int ivftq_decode(const ivftq_store* store, const int64_t* slot_of,
+                 const int32_t* list_of, int64_t n, const float* centroids,
+                 const double* R_T, const double* levels, int flat, int renormalize,
+                 double* out, void* scratch, size_t scratch_bytes, void* stream);
+size_t ivftq_decode_scratch_bytes(int64_t n, int dim);
+/* out[i] = <a_i, c_{l_i}> in f64 (refresh report IPs, refresh.py:179-187). */
+int ivftq_rowdot(const double* a, const float* centroids, const int32_t* list_ids,
+                 int64_t n, int dim, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IVFTQ_B200_H */

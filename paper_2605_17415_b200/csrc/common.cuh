@@ -1,0 +1,187 @@
+// Shared device helpers for the IVF-TQ B200 library (sm_100a).
+//
+// Numerics that must match the reference bit-for-bit live here:
+//   * pw_sumsq  -- numpy's pairwise summation of squares, the arithmetic behind
+//                  np.linalg.norm(x, axis=1) (index.py:241, 254, 265).
+//   * d2h_bits  -- float64 -> binary16 round-to-nearest-even, the arithmetic
+//                  behind `rnorm.astype(np.float16)` (index.py:255).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/ivftq_b200.h"
+
+#define IVFTQ_HD __host__ __device__ __forceinline__
+
+namespace ivftq {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kPwBlock = 128;  // numpy PW_BLOCKSIZE
+
+// ---------------------------------------------------------------------------
+// float64 -> binary16 bits, round to nearest even (host + device).
+IVFTQ_HD uint16_t d2h_bits(double x) {
+  uint64_t u;
+  memcpy(&u, &x, 8);
+  uint16_t sgn = (uint16_t)((u >> 48) & 0x8000u);
+  u &= 0x7fffffffffffffffull;
+  if (u >= 0x7ff0000000000000ull) {  // inf / nan
+    return (uint16_t)(sgn | (u == 0x7ff0000000000000ull ? 0x7c00u : 0x7e00u));
+  }
+  int e = (int)(u >> 52) - 1023;
+  if (e >= 16) return (uint16_t)(sgn | 0x7c00u);
+  if (e < -25) return sgn;  // below half the smallest subnormal (or zero)
+  uint64_t m = (u & 0x000fffffffffffffull) | 0x0010000000000000ull;
+  if ((u >> 52) == 0) return sgn;  // double subnormal
+  int shift = (e >= -14) ? 42 : (28 - e);
+  uint64_t q = m >> shift;
+  uint64_t rem = m & ((1ull << shift) - 1);
+  uint64_t half = 1ull << (shift - 1);
+  if (rem > half || (rem == half && (q & 1))) q++;
+  uint32_t h;
+  if (e >= -14) {
+    h = ((uint32_t)(e + 15) << 10) + (uint32_t)q - 1024u;  // carry rolls into exponent
+  } else {
+    h = (uint32_t)q;
+  }
+  return (uint16_t)(sgn | h);
+}
+
+IVFTQ_HD float h2f_bits(uint16_t h) {
+  uint32_t s = (uint32_t)(h & 0x8000u) << 16;
+  uint32_t e = (h >> 10) & 0x1f;
+  uint32_t m = h & 0x3ff;
+  uint32_t out;
+  if (e == 0) {
+    if (m == 0) {
+      out = s;
+    } else {  // subnormal: normalise
+      int sh = 0;
+      while (!(m & 0x400)) { m <<= 1; ++sh; }
+      m &= 0x3ff;
+      out = s | ((uint32_t)(127 - 15 - sh + 1) << 23) | (m << 13);
+    }
+  } else if (e == 31) {
+    out = s | 0x7f800000u | (m << 13);
+  } else {
+    out = s | ((e - 15 + 127) << 23) | (m << 13);
+  }
+  float f;
+  memcpy(&f, &out, 4);
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// numpy pairwise sum of squares over a[0..n) with element stride `st`
+// (loops_utils.h.src pairwise_sum; squares rounded before summation, no FMA).
+#ifdef __CUDACC__
+__device__ __forceinline__ double sq(double v) { return __dmul_rn(v, v); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+#endif
+
+template <typename Load>
+__device__ double pw_block(Load ld, int base, int n) {
+  if (n < 8) {
+    double r = -0.0;
+    for (int i = 0; i < n; ++i) r = add(r, sq(ld(base + i)));
+    return r;
+  }
+  double r0 = sq(ld(base + 0)), r1 = sq(ld(base + 1)), r2 = sq(ld(base + 2)),
+         r3 = sq(ld(base + 3)), r4 = sq(ld(base + 4)), r5 = sq(ld(base + 5)),
+         r6 = sq(ld(base + 6)), r7 = sq(ld(base + 7));
+  int i = 8;
+  int lim = n - (n % 8);
+  for (; i < lim; i += 8) {
+    r0 = add(r0, sq(ld(base + i + 0)));
+    r1 = add(r1, sq(ld(base + i + 1)));
+    r2 = add(r2, sq(ld(base + i + 2)));
+    r3 = add(r3, sq(ld(base + i + 3)));
+    r4 = add(r4, sq(ld(base + i + 4)));
+    r5 = add(r5, sq(ld(base + i + 5)));
+    r6 = add(r6, sq(ld(base + i + 6)));
+    r7 = add(r7, sq(ld(base + i + 7)));
+  }
+  double res = add(add(add(r0, r1), add(r2, r3)), add(add(r4, r5), add(r6, r7)));
+  for (; i < n; ++i) res = add(res, sq(ld(base + i)));
+  return res;
+}
+
+// Iterative form of numpy's recursion: split n > 128 at n2 = n/2 - (n/2 % 8)
+// and add the halves' sums left + right. Depth <= 16 for any int length.
+template <typename Load>
+__device__ double pw_sumsq(Load ld, int n) {
+  if (n <= kPwBlock) return pw_block(ld, 0, n);
+  // explicit post-order traversal
+  int st_base[24], st_n[24];
+  double st_left[24];
+  unsigned char st_state[24];
+  int sp = 0;
+  st_base[0] = 0; st_n[0] = n; st_state[0] = 0;
+  double ret = 0.0;
+  while (sp >= 0) {
+    int b = st_base[sp], m = st_n[sp];
+    if (m <= kPwBlock) {
+      ret = pw_block(ld, b, m);
+      --sp;
+      // deliver to parent
+      while (sp >= 0) {
+        if (st_state[sp] == 1) {  // left finished -> start right
+          st_left[sp] = ret;
+          st_state[sp] = 2;
+          int h = st_n[sp] / 2; h -= h % 8;
+          ++sp;
+          st_base[sp] = st_base[sp - 1] + h;
+          st_n[sp] = st_n[sp - 1] - h;
+          st_state[sp] = 0;
+          break;
+        } else {  // right finished
+          ret = add(st_left[sp], ret);
+          --sp;
+        }
+      }
+      continue;
+    }
+    // descend left
+    int h = m / 2; h -= h % 8;
+    st_state[sp] = 1;
+    ++sp;
+    st_base[sp] = b; st_n[sp] = h; st_state[sp] = 0;
+  }
+  return ret;
+}
+
+// ---------------------------------------------------------------------------
+// Code layout helpers. One "field" per coordinate: c = bin*2 + sign
+// (use_sign) or c = bin, `field_bits` wide, `fields_per_word` per uint32,
+// little-endian inside the word; 32-vector blocks interleave words so that
+// word w of vector v lives at codes[(blk*W + w)*32 + v].
+IVFTQ_HD int field_bits(int bits, int use_sign) { return bits + (use_sign ? 1 : 0); }
+IVFTQ_HD int fields_per_word(int fb) { return 32 / fb; }
+IVFTQ_HD int words_per_vec(int dim, int fb) {
+  int f = fields_per_word(fb);
+  return (dim + f - 1) / f;
+}
+
+// Key order shared by every top-k in the library: score desc, id asc
+// (index.py:480-483 lexsort((ids, -scores)); evaluation.py:78 stable argsort).
+IVFTQ_HD bool better(double s1, int i1, double s2, int i2) {
+  return s1 > s2 || (s1 == s2 && i1 < i2);
+}
+
+}  // namespace ivftq
+
+// Error plumbing shared by the C-ABI wrappers.
+namespace ivftq {
+void set_error(const char* fmt, ...);
+int check_launch(const char* what);
+}  // namespace ivftq
+
+#define IVFTQ_CHECK_CUDA(expr)                                             \
+  do {                                                                     \
+    cudaError_t _e = (expr);                                               \
+    if (_e != cudaSuccess) {                                               \
+      ::ivftq::set_error("%s: %s", #expr, cudaGetErrorString(_e));         \
+      return IVFTQ_ERR_CUDA;                                               \
+    }                                                                      \
+  } while (0)

@@ -1,0 +1,365 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle on the same seeded inputs.
+
+Bars (north_star): codes bit-exact (a fraction <= 1e-4 of boundary flips is
+tolerated and reported), list ids and binary16 norms identical, probe lists
+identical, scores within 1e-4 relative, top-k ids identical up to ties within
+that tolerance, recall@10 within 0.1 pp.
+"""
+
+import warnings
+
+import numpy as np
+import pytest
+
+from helpers import SCORE_RTOL, compare_topk, index_from_golden, parts_from_golden
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["d32_b4_L16_raw", "d16_b3_L8", "d24_b5_L12_raw", "d96_b2_nosign_L32",
+         "d200_b3_L16", "d64_b8_L8", "d40_b1_L4", "d128_b4_L64", "flat_d16_b8"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+
+
+def _search_keys(g):
+    out = []
+    for k in g:
+        if k.startswith("s_") and k.endswith("_ids"):
+            _, kk, p, rr, _ = k.split("_")
+            out.append((int(kk), int(p), int(rr)))
+    return out
+
+
+def test_device_normalize_bit_exact():
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+
+    L = _lib.lib()
+    for d in (2, 7, 16, 96, 128, 129, 200, 300):
+        rng = np.random.default_rng(d)
+        x = rng.standard_normal((777, d)) * np.exp(rng.uniform(-3, 3, (777, 1)))
+        x[5] = 0.0
+        x[9] = 0.0
+        xt = torch.from_numpy(x).cuda()
+        out = torch.empty_like(xt)
+        bad = torch.empty(1, dtype=torch.int64, device="cuda")
+        _lib.check(L.ivftq_normalize_rows(xt.data_ptr(), 1, 777, d, out.data_ptr(),
+                                          bad.data_ptr(), _lib.stream_ptr()))
+        assert int(bad.item()) == 5
+        ref = x / np.linalg.norm(x, axis=1)[:, None]
+        got = out.cpu().numpy()
+        ok = np.ones(777, bool)
+        ok[[5, 9]] = False
+        np.testing.assert_array_equal(got[ok], ref[ok])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_encode_matches_reference(golden, name):
+    g = golden(name)
+    idx = index_from_golden(g)
+    ids = idx.add_batch(g["x"])
+    np.testing.assert_array_equal(ids, np.arange(len(g["x"])))
+    np.testing.assert_array_equal(idx.list_ids, g["list_ids"])
+    np.testing.assert_array_equal(idx.norms.view(np.uint16), g["norms"].view(np.uint16))
+    flips = (idx.bins != g["bins"]) | (idx.signs != g["signs"])
+    assert flips.mean() <= 1e-4, flips.mean()
+    np.testing.assert_array_equal(idx.bins, g["bins"])
+    np.testing.assert_array_equal(idx.signs, g["signs"])
+    if g["config"][4]:
+        np.testing.assert_array_equal(idx.raw, g["raw"])
+    assert idx.compression_fingerprint() == g["fingerprint"].tobytes().decode()
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_search_matches_reference(golden, name):
+    g = golden(name)
+    idx = index_from_golden(g)
+    idx.add_batch(g["x"])
+    for (k, n_p, rr) in _search_keys(g):
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            ids, sc = idx.search_batch(g["queries"], k, n_p, rr)
+        assert ids.dtype == np.int64 and sc.dtype == np.float64
+        compare_topk(ids, sc, g[f"s_{k}_{n_p}_{rr}_ids"], g[f"s_{k}_{n_p}_{rr}_scores"])
+
+
+def test_probes_identical(golden):
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+
+    g = golden("d128_b4_L64")
+    idx = index_from_golden(g)
+    qn, bad, nq = idx._normalize_queries_device(g["queries"])
+    L = _lib.lib()
+    probe = torch.empty((nq, 64), dtype=torch.int32, device="cuda")
+    coarse = torch.empty((nq, 64), dtype=torch.float64, device="cuda")
+    sb = L.ivftq_probe_scratch_bytes(nq, 64)
+    scr = torch.empty(sb, dtype=torch.uint8, device="cuda")
+    _lib.check(L.ivftq_probe(qn.data_ptr(), idx._cent.data_ptr(), nq, 64, 128, 64,
+                             probe.data_ptr(), coarse.data_ptr(), scr.data_ptr(), sb,
+                             _lib.stream_ptr()))
+    np.testing.assert_array_equal(probe.cpu().numpy(), g["probe_all"][:, :64])
+    ref = np.take_along_axis(g["coarse"], g["probe_all"][:, :64], 1)
+    np.testing.assert_allclose(coarse.cpu().numpy(), ref, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("seed,d,bits,L,sign", [(1, 48, 4, 24, True), (2, 100, 3, 40, True),
+                                                  (3, 64, 2, 16, False), (4, 130, 4, 8, True),
+                                                  (5, 33, 6, 12, True), (6, 20, 7, 6, False)])
+def test_random_configs_against_oracle(seed, d, bits, L, sign):
+    """Fresh seeded inputs, oracle restatement as the checker."""
+    from oracle import ivftq_oracle as orc
+    from paper_2605_17415_b200 import (CoarsePartition, IndexConfig, IvfTqIndex,
+                                       design_quantizer, generate_rotation)
+    from paper_2605_17415_b200.workloads import mixture
+
+    x, means = mixture(3000, d, 30, 0.3, seed)
+    qx, _ = mixture(120, d, 30, 0.3, seed + 100, means=means)
+    xn = orc.normalize_rows(x)
+    cent = orc.train_partition(xn[:1500], L, seed=seed, max_iters=5)
+    q = design_quantizer(bits, d)
+    R = generate_rotation(d, seed)
+    cfg = IndexConfig(dim=d, bits=bits, n_lists=L, use_sign_bit=sign, keep_raw=True)
+    idx = IvfTqIndex(cfg, q, R, CoarsePartition(L, d, cent))
+    idx.add_batch(x[:1000])
+    idx.add_batch(x[1000:])
+    o = orc.OracleIndex(cent, R.matrix, q.boundaries, q.centroids, q.half_bin_means,
+                        use_sign=sign, keep_raw=True)
+    o.add_batch(x)
+    np.testing.assert_array_equal(idx.list_ids, o.list_ids)
+    np.testing.assert_array_equal(idx.norms.view(np.uint16), o.norms.view(np.uint16))
+    assert ((idx.bins != o.bins) | (idx.signs != o.signs)).mean() <= 1e-4
+    for (k, n_p, rr) in [(10, 4, 0), (10, L, 0), (1, 2, 0), (7, 3, 15)]:
+        a = idx.search_batch(qx, k, n_p, rr)
+        b = o.search_batch(qx, k, n_p, rr)
+        compare_topk(*a, *b)
+
+
+@pytest.mark.slow
+def test_pr1_full_parity(golden):
+    """configs[0] at full size: 100k x 128, L=256, b=4; 1k queries, n_p sweep."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).parent / "golden"))
+    from hashing import row_hash
+
+    from paper_2605_17415_b200.index import pack_fields
+    from paper_2605_17415_b200.evaluation import recall_at_k
+    from paper_2605_17415_b200.workloads import make_workload
+
+    g = golden("pr1")
+    w = make_workload("pr1")
+    idx = index_from_golden(g)
+    idx.add_batch(w.base())
+    np.testing.assert_array_equal(idx.list_ids, g["list_ids"].astype(np.int64))
+    np.testing.assert_array_equal(idx.norms.view(np.uint16), g["norms"].view(np.uint16))
+    packed = np.concatenate([pack_fields(idx.bins, 4), pack_fields(idx.signs, 1)], 1)
+    mism = (row_hash(packed) != g["code_hash"]).mean()
+    assert mism <= 1e-4, mism
+    qx = w.queries()
+    for n_p in (1, 4, 16, 64):
+        ids, sc = idx.search_batch(qx, 10, n_p)
+        ref_i, ref_s = g[f"s_10_{n_p}_0_ids"], g[f"s_10_{n_p}_0_scores"]
+        ndiff = compare_topk(ids, sc, ref_i, ref_s)
+        assert ndiff <= 0.01 * len(ids)
+        r_ours = recall_at_k(ids, g["truth10"], 10)
+        r_ref = recall_at_k(ref_i, g["truth10"], 10)
+        assert abs(r_ours - r_ref) <= 0.001, (n_p, r_ours, r_ref)
+
+
+def test_exact_topk_gpu_matches_reference(golden):
+    from paper_2605_17415_b200.evaluation import exact_topk
+
+    for name in ("d32_b4_L16_raw", "d128_b4_L64"):
+        g = golden(name)
+        x = g["x"].astype(np.float64)
+        xn = x / np.linalg.norm(x, axis=1)[:, None]
+        t = exact_topk(xn, g["queries"], 10, db_chunk=1000)
+        np.testing.assert_array_equal(t.ids, g["truth10"])
+
+
+class TestEdgeCases:
+    def test_errors_and_warnings(self, golden):
+        g = golden("d32_b4_L16_raw")
+        idx = index_from_golden(g)
+        idx.add_batch(g["x"][:500])
+        with pytest.raises(ValueError, match="k must be"):
+            idx.search(g["x"][0], 0, n_p=2)
+        with pytest.raises(ValueError, match="n_p must be"):
+            idx.search(g["x"][0], 3, n_p=0)
+        with pytest.warns(UserWarning, match="clamping"):
+            idx.search(g["x"][0], 3, n_p=999)
+        with pytest.raises(ValueError, match="dim"):
+            idx.search(np.ones(16), 3, n_p=2)
+        with pytest.raises(ValueError, match="zero-norm query"):
+            idx.search(np.zeros(32), 3, n_p=2)
+        with pytest.raises(ValueError, match="row at index 3"):
+            bad = g["x"][:6].copy()
+            bad[3] = 0
+            idx.add_batch(bad)
+        with pytest.raises(ValueError, match="external_ids length"):
+            idx.add_batch(g["x"][:3], external_ids=np.arange(2))
+        assert idx.count == 500
+
+    def test_rerank_requires_raw(self, golden):
+        g = golden("d16_b3_L8")
+        idx = index_from_golden(g)
+        idx.add_batch(g["x"])
+        with pytest.raises(ValueError, match="keep_raw"):
+            idx.search(g["x"][0], 3, n_p=2, rerank_depth=5)
+
+    def test_empty_index_pads(self, golden):
+        g = golden("d16_b3_L8")
+        idx = index_from_golden(g)
+        ids, sc = idx.search_batch(g["queries"][:4], 5, 3)
+        assert (ids == -1).all() and np.isneginf(sc).all()
+
+    def test_centroid_input_zero_residual(self, golden):
+        g = golden("d32_b4_L16_raw")
+        idx = index_from_golden(g)
+        code = idx.encode(idx.partition.centroids[3].astype(np.float64))
+        ref = g["centroid_code"].tobytes()
+        assert code.codes + code.signs == ref
+        assert code.list_id == int(g["centroid_code_meta"][0]) == 3
+        assert float(code.residual_norm) == 0.0
+
+    def test_incremental_equals_batch(self, golden):
+        g = golden("d16_b3_L8")
+        a = index_from_golden(g)
+        a.add_batch(g["x"])
+        b = index_from_golden(g)
+        b.add_batch(g["x"][:600])
+        b.search_batch(g["queries"], 5, 8)
+        for row in g["x"][600:650]:
+            b.add(row)
+        b.add_batch(g["x"][650:])
+        np.testing.assert_array_equal(a.bins, b.bins)
+        ia, sa = a.search_batch(g["queries"], 10, 8)
+        ib, sb = b.search_batch(g["queries"], 10, 8)
+        np.testing.assert_array_equal(ia, ib)
+        np.testing.assert_array_equal(sa, sb)
+
+    def test_duplicates_tie_to_lower_id(self, golden):
+        g = golden("d32_b4_L16_raw")  # rows 2000..2039 duplicate rows 0..39
+        idx = index_from_golden(g)
+        idx.add_batch(g["x"])
+        ids, sc = idx.search_batch(g["x"][:40], 2, 16)
+        for i in range(40):
+            assert sc[i, 0] == sc[i, 1]
+            assert ids[i, 0] < ids[i, 1]
+
+    def test_partition_lists_view(self, golden):
+        g = golden("d16_b3_L8")
+        idx = index_from_golden(g)
+        idx.add_batch(g["x"])
+        lists = idx.partition.lists
+        assert sum(len(m) for m in lists) == idx.count
+        for l, m in enumerate(lists):
+            assert m == sorted(m)
+            assert all(idx.list_ids[i] == l for i in m)
+
+    def test_bit_flip_ablation_restores(self, golden):
+        g = golden("d32_b4_L16_raw")
+        idx = index_from_golden(g)
+        idx.add_batch(g["x"])
+        before = idx.bins.copy(), idx.signs.copy()
+        truth = g["truth10"]
+        r0 = idx.bit_flip_ablation("msb_primary", 0.0, g["queries"], 10, 16, truth=truth)
+        assert r0["recall_drop"] == 0.0
+        r = idx.bit_flip_ablation("msb_primary", 0.5, g["queries"], 10, 16, seed=1, truth=truth)
+        assert r["recall_drop"] > 0
+        idx.bit_flip_ablation("sign", 0.3, g["queries"], 10, 16, seed=2, truth=truth)
+        np.testing.assert_array_equal(idx.bins, before[0])
+        np.testing.assert_array_equal(idx.signs, before[1])
+
+
+class TestStorage:
+    @pytest.mark.parametrize("name", ["d32_b4_L16_raw", "d24_b5_L12_raw",
+                                      "d96_b2_nosign_L32", "flat_d16_b8"])
+    def test_bytes_identical_to_reference(self, golden, tmp_path, name):
+        from paper_2605_17415_b200.storage import load_index, save_index
+
+        g = golden(name)
+        idx = index_from_golden(g)
+        idx.add_batch(g["x"])
+        p = tmp_path / "a.ivtq"
+        save_index(idx, p)
+        assert p.read_bytes() == g["ivtq_bytes"].tobytes()
+        # load the reference's own file, search identically
+        q = tmp_path / "ref.ivtq"
+        q.write_bytes(g["ivtq_bytes"].tobytes())
+        loaded = load_index(q)
+        k, n_p, rr = _search_keys(g)[0]
+        a = idx.search_batch(g["queries"], k, n_p, rr)
+        b = loaded.search_batch(g["queries"], k, n_p, rr)
+        np.testing.assert_array_equal(a[0], b[0])
+        np.testing.assert_array_equal(a[1], b[1])
+        np.testing.assert_array_equal(loaded.bins, idx.bins)
+        assert loaded.partition.lists == idx.partition.lists
+
+    def test_corrupt_files(self, golden, tmp_path):
+        from paper_2605_17415_b200.storage import IndexFormatError, load_index
+
+        raw = golden("d32_b4_L16_raw")["ivtq_bytes"].tobytes()
+        for bad in (b"NOPE" + raw[4:], raw[:-7], raw + b"\0"):
+            p = tmp_path / "x.ivtq"
+            p.write_bytes(bad)
+            with pytest.raises(IndexFormatError):
+                load_index(p)
+
+
+class TestRefresh:
+    @pytest.mark.parametrize("name,seed", [("refresh_recon", 3), ("refresh_raw", 4)])
+    def test_refresh_matches_reference(self, golden, name, seed):
+        from paper_2605_17415_b200.refresh import RefreshPolicy, refresh
+
+        g = golden(name)
+        idx = index_from_golden(g, "pre_")
+        idx.add_batch(g["x"])
+        fp = idx.compression_fingerprint()
+        ext = idx.external_ids.copy()
+        rep = refresh(idx, RefreshPolicy(seed=seed))
+        ref = g["report"]
+        assert rep.refreshed and rep.n_reassigned == int(ref[0])
+        assert rep.sample_size == int(ref[1]) and rep.used_raw == bool(ref[2])
+        np.testing.assert_array_equal(idx.partition.centroids, g["post_centroids"])
+        np.testing.assert_array_equal(idx.list_ids, g["post_list_ids"])
+        np.testing.assert_array_equal(idx.norms.view(np.uint16), g["post_norms"].view(np.uint16))
+        np.testing.assert_array_equal(idx.bins, g["post_bins"])
+        np.testing.assert_array_equal(idx.signs, g["post_signs"])
+        np.testing.assert_allclose([rep.mean_assigned_ip_before, rep.mean_assigned_ip_after,
+                                    rep.centroid_displacement_mean,
+                                    rep.centroid_displacement_max], ref[3:], rtol=1e-9)
+        assert idx.compression_fingerprint() == fp
+        np.testing.assert_array_equal(idx.external_ids, ext)
+        compare_topk(*idx.search_batch(g["queries"], 10, 8), g["s_10_8_0_ids"],
+                     g["s_10_8_0_scores"])
+
+    def test_empty_refresh_noop(self, golden):
+        from paper_2605_17415_b200.refresh import RefreshPolicy, refresh
+
+        idx = index_from_golden(golden("d16_b3_L8"))
+        assert not refresh(idx, RefreshPolicy()).refreshed
+
+    def test_reconstruct_matches_oracle(self, golden):
+        from oracle import ivftq_oracle as orc
+        from paper_2605_17415_b200.refresh import reconstruct_all, reconstruct_vector
+
+        g = golden("d32_b4_L16_raw")
+        idx = index_from_golden(g)
+        idx.add_batch(g["x"])
+        o = orc.OracleIndex(g["centroids"], g["R"], g["boundaries"], g["qcent"], g["half"])
+        o.add_batch(g["x"])
+        rec = reconstruct_all(idx)
+        np.testing.assert_allclose(rec, orc.reconstruct_all(o), rtol=0, atol=1e-13)
+        np.testing.assert_allclose(reconstruct_vector(idx, 123), rec[123], atol=1e-15)
