@@ -41,9 +41,10 @@ extern "C" {
  * List l owns slots [list_offset[l], list_offset[l] + list_cap[l]); offsets and
  * capacities are multiples of 128 slots. Codes of 32 consecutive slots form a
  * block: word w of slot s is codes[((s/32)*words_per_vec + w)*32 + s%32].
- * Each word packs `fields_per_word` coordinates of field_bits = bits+use_sign
- * bits (field value bin*2+sign, or bin), coordinate j of the word at bit
- * field_bits*j. Slot order inside a list is arbitrary: every result is
+ * Each word packs `fields_per_word` coordinates of field_bits = bits+1 bits
+ * (field value bin*2+sign; the sign is stored even when use_sign is 0, as the
+ * reference stores `signs` unconditionally), coordinate j of the word at bit
+ * field_bits*j. levels[] tables are indexed by the field value. Slot order inside a list is arbitrary: every result is
  * ordered by (score desc, internal id asc), never by slot. */
 typedef struct ivftq_store {
   int32_t dim;

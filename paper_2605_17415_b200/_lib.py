@@ -94,7 +94,7 @@ def load(path: str | os.PathLike | None = None):
     global _LIB
     if _LIB is not None and path is None:
         return _LIB
-    p = Path(path) if path else LIB_PATH
+    p = Path(path) if path else Path(os.environ.get("IVFTQ_LIB", LIB_PATH))
     if not p.exists():
         raise FileNotFoundError(
             f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")

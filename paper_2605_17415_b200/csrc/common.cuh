@@ -14,6 +14,24 @@
 
 #define IVFTQ_HD __host__ __device__ __forceinline__
 
+// Device bounds checks, compiled in only for the debug build (make debug).
+#ifdef IVFTQ_DEBUG
+#include <cstdio>
+#define DCHECK(cond, ...)                                                      \
+  do {                                                                         \
+    if (!(cond)) {                                                             \
+      printf("DCHECK %s:%d %s | ", __FILE__, __LINE__, #cond);                 \
+      printf(__VA_ARGS__);                                                     \
+      printf("\n");                                                            \
+      __trap();                                                                \
+    }                                                                          \
+  } while (0)
+#else
+#define DCHECK(cond, ...) \
+  do {                    \
+  } while (0)
+#endif
+
 namespace ivftq {
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -152,11 +170,14 @@ __device__ double pw_sumsq(Load ld, int n) {
 }
 
 // ---------------------------------------------------------------------------
-// Code layout helpers. One "field" per coordinate: c = bin*2 + sign
-// (use_sign) or c = bin, `field_bits` wide, `fields_per_word` per uint32,
+// Code layout helpers. One "field" per coordinate: c = bin*2 + sign,
+// `field_bits` = bits + 1 wide, `fields_per_word` per uint32. The sign bit is
+// stored even when scoring ignores it: the reference keeps it in `signs` and
+// in .ivtq files regardless of use_sign_bit (index.py:266, storage.py:283);
+// without the sign the level table simply maps both halves to the centroid.
 // little-endian inside the word; 32-vector blocks interleave words so that
 // word w of vector v lives at codes[(blk*W + w)*32 + v].
-IVFTQ_HD int field_bits(int bits, int use_sign) { return bits + (use_sign ? 1 : 0); }
+IVFTQ_HD int field_bits(int bits, int /*use_sign*/) { return bits + 1; }
 IVFTQ_HD int fields_per_word(int fb) { return 32 / fb; }
 IVFTQ_HD int words_per_vec(int dim, int fb) {
   int f = fields_per_word(fb);

@@ -71,16 +71,13 @@ residual_kernel(const double* __restrict__ xn, const float* __restrict__ cent,
 
 // bin = #interior boundaries <= v (upper-bin on ties), sign = v >= centroid.
 __device__ __forceinline__ uint32_t quant_field(double v, const double* bnd,
-                                                const double* qc, int levels,
-                                                int use_sign) {
+                                                const double* qc, int levels) {
   int lo = 0, hi = levels - 1;
   while (lo < hi) {
     int mid = (lo + hi + 1) >> 1;
     if (bnd[mid] <= v) lo = mid; else hi = mid - 1;
   }
-  uint32_t c = (uint32_t)lo;
-  if (use_sign) c = (c << 1) | (v >= qc[lo] ? 1u : 0u);
-  return c;
+  return ((uint32_t)lo << 1) | (v >= qc[lo] ? 1u : 0u);
 }
 
 __global__ void __launch_bounds__(kRowThreads)
@@ -121,7 +118,7 @@ quantize_pack_kernel(const double* __restrict__ rot, const uint16_t* __restrict_
         int j = w * fpw + f;
         if (j >= d) break;
         double u = __ddiv_rn(rp[j], nr);
-        word |= quant_field(u, bnd, qc, levels, use_sign) << (fb * f);
+        word |= quant_field(u, bnd, qc, levels) << (fb * f);
       }
     }
     words[(row0 + r) * W + w] = word;
@@ -141,8 +138,7 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ bins,
   for (int f = 0; f < fpw; ++f) {
     int j = w * fpw + f;
     if (j >= d) break;
-    uint32_t c = bins[r * d + j];
-    if (use_sign) c = (c << 1) | (signs[r * d + j] & 1u);
+    uint32_t c = ((uint32_t)bins[r * d + j] << 1) | (signs[r * d + j] & 1u);
     word |= c << (fb * f);
   }
   words[i] = word;
@@ -207,13 +203,8 @@ __global__ void export_codes_kernel(ivftq_store s, const int64_t* __restrict__ s
     int j = w * fpw + f;
     if (j >= d) break;
     uint32_t c = (word >> (fb * f)) & mask;
-    if (s.use_sign) {
-      bins[r * d + j] = (uint8_t)(c >> 1);
-      if (signs) signs[r * d + j] = (uint8_t)(c & 1u);
-    } else {
-      bins[r * d + j] = (uint8_t)c;
-      if (signs) signs[r * d + j] = 0;
-    }
+    bins[r * d + j] = (uint8_t)(c >> 1);
+    if (signs) signs[r * d + j] = (uint8_t)(c & 1u);
   }
 }
 
@@ -232,7 +223,7 @@ __global__ void xor_codes_kernel(ivftq_store s, const int64_t* __restrict__ slot
     int j = w * fpw + f;
     if (j >= d) break;
     if (mask[r * d + j]) {
-      uint32_t v = (which == 1) ? 1u : (uint32_t)flip << (s.use_sign ? 1 : 0);
+      uint32_t v = (which == 1) ? 1u : (uint32_t)flip << 1;
       x |= v << (fb * f);
     }
   }
@@ -361,10 +352,6 @@ extern "C" int ivftq_export_codes(const ivftq_store* store, const int64_t* slot_
 extern "C" int ivftq_xor_codes(const ivftq_store* store, const int64_t* slot_of, int64_t n,
                                const uint8_t* mask, int which, int flip, void* stream) {
   if (n == 0) return 0;
-  if (which == 1 && !store->use_sign) {
-    set_error("sign flips need use_sign");
-    return IVFTQ_ERR_ARG;
-  }
   int64_t tot = n * store->words_per_vec;
   xor_codes_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, S(stream)>>>(
       *store, slot_of, n, mask, which, flip);

@@ -110,10 +110,15 @@ scan_lut_kernel(ivftq_store st, const int32_t* __restrict__ probe,
     int vid = 0;
     if (item < total) {
       while (pref[t + 1] <= item) ++t;
+      DCHECK(t < np_b, "t=%d np_b=%d item=%d total=%d", t, np_b, item, total);
       int l = pl[t];
+      DCHECK(l >= 0 && l < st.n_lists, "l=%d t=%d q=%lld", l, t, (long long)q);
       int blk = item - pref[t];
       int size = st.list_size[l];
       int64_t off = st.list_offset[l];
+      DCHECK(off >= 0 && off + (int64_t)blk * 32 + 32 <= st.capacity + 32,
+             "off=%lld blk=%d size=%d cap=%lld", (long long)off, blk, size,
+             (long long)st.capacity);
       int64_t gblk = (off >> 5) + blk;
       bool valid = blk * 32 + lane < size;
       if (valid) {

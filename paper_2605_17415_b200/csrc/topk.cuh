@@ -68,6 +68,7 @@ struct BlockTopK {
     base = __shfl_sync(kFull, base, leader);
     if (pass) {
       int pos = base + __popc(m & ((1u << lane) - 1u));
+      DCHECK(pos < cap, "push pos=%d cap=%d", pos, cap);
       s[pos] = sc;
       id[pos] = i;
     }
@@ -78,6 +79,7 @@ struct BlockTopK {
     __syncthreads();
     int n = *cnt;
     int P = pow2ceil(n > 1 ? n : 1);
+    DCHECK(P <= cap, "merge n=%d cap=%d", n, cap);
     for (int i = n + threadIdx.x; i < P; i += blockDim.x) {
       s[i] = -INFINITY;
       id[i] = INT_MAX;
@@ -114,7 +116,11 @@ struct BlockTopK {
   // call after a round's pushes (all threads)
   __device__ void round_end(int round) {
     __syncthreads();
-    if (*(volatile int*)cnt > cap - round) merge();
+    int c = *(volatile int*)cnt;
+    // second barrier: nobody may push for the next round before every thread
+    // has read the count, or the merge decision would diverge across warps
+    __syncthreads();
+    if (c > cap - round) merge();
   }
 };
 

@@ -141,11 +141,11 @@ class IvfTqIndex:
             "cuda", torch.cuda.current_device())
         d = config.dim
         dev = self.device
-        self._R = torch.from_numpy(np.ascontiguousarray(rot.matrix, np.float64)).to(dev)
-        self._RT = torch.from_numpy(np.ascontiguousarray(rot.matrix.T, np.float64)).to(dev)
-        self._bnd = torch.from_numpy(np.ascontiguousarray(quantizer.boundaries, np.float64)).to(dev)
-        self._qcent = torch.from_numpy(np.ascontiguousarray(quantizer.centroids, np.float64)).to(dev)
-        self._levels = torch.from_numpy(quantizer.levels(config.use_sign_bit)).to(dev)
+        self._R = torch.from_numpy(np.array(rot.matrix, np.float64)).to(dev)
+        self._RT = torch.from_numpy(np.array(rot.matrix.T, np.float64, order="C")).to(dev)
+        self._bnd = torch.from_numpy(np.array(quantizer.boundaries, np.float64)).to(dev)
+        self._qcent = torch.from_numpy(np.array(quantizer.centroids, np.float64)).to(dev)
+        self._levels = torch.from_numpy(np.array(quantizer.levels(config.use_sign_bit), order="C")).to(dev)
         self._store = DeviceStore(d, config.bits, config.use_sign_bit, partition.n_lists, dev)
         self._slot_of = _Grow((), torch.int64, dev, -1)
         self._list_of = _Grow((), torch.int32, dev, 0)
@@ -243,9 +243,7 @@ class IvfTqIndex:
         f = np.arange(d)
         word_idx, fld = f // s.fields_per_word, f % s.fields_per_word
         vals = (w[:, word_idx] >> (s.field_bits * fld).astype(np.uint32)) & ((1 << s.field_bits) - 1)
-        if s.use_sign:
-            return (vals >> 1).astype(np.uint8), (vals & 1).astype(np.uint8)
-        return vals.astype(np.uint8), np.zeros((n, d), np.uint8)
+        return (vals >> 1).astype(np.uint8), (vals & 1).astype(np.uint8)
 
     def _encode_batch(self, x: np.ndarray, partition: CoarsePartition | None = None):
         """Host-visible encode (index.py:231-267): (bins, signs, list_ids, f16 norms, xn)."""

@@ -97,8 +97,14 @@ class ScalarQuantizer:
         return self.half_bin_means if use_sign else self.centroids
 
     def levels(self, use_sign: bool) -> np.ndarray:
-        """Flattened table indexed by the device field value bin*2+sign (or bin)."""
-        return np.ascontiguousarray(self.reconstruction_table(use_sign), dtype=np.float64).ravel()
+        """Flattened f64 table indexed by the device field value bin*2+sign.
+
+        Without the sign bit both halves of a bin map to its centroid, which is
+        `reconstruction_table(False)[bin]` (lloydmax.py:146-150).
+        """
+        if use_sign:
+            return np.ascontiguousarray(self.half_bin_means, dtype=np.float64).ravel()
+        return np.repeat(np.asarray(self.centroids, dtype=np.float64), 2)
 
 
 def design_quantizer(bits: int, dim: int, tol: float = 1e-10,

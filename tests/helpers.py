@@ -3,6 +3,10 @@
 import numpy as np
 
 SCORE_RTOL = 1e-4  # north_star: estimated scores within 1e-4 relative
+# absolute floor for scores near 0: the reference's own f32 residual GEMM
+# (index.py:453) carries ~d * 2^-24 absolute error, so a relative bound is
+# meaningless for |score| << 1e-2.
+SCORE_ATOL = 1e-6
 
 
 def parts_from_golden(g, prefix=""):
@@ -32,7 +36,7 @@ def index_from_golden(g, prefix=""):
     return IvfTqIndex(cfg, q, rot, part)
 
 
-def compare_topk(ids, scores, ref_ids, ref_scores, rtol=SCORE_RTOL):
+def compare_topk(ids, scores, ref_ids, ref_scores, rtol=SCORE_RTOL, atol=SCORE_ATOL):
     """Assert top-k parity up to ties within rtol; return #queries that differ."""
     ids = np.asarray(ids)
     ref_ids = np.asarray(ref_ids)
@@ -40,7 +44,7 @@ def compare_topk(ids, scores, ref_ids, ref_scores, rtol=SCORE_RTOL):
     fin = np.isfinite(ref_scores)
     np.testing.assert_array_equal(np.isfinite(scores), fin)
     np.testing.assert_array_equal(ids[~fin], -1)
-    np.testing.assert_allclose(scores[fin], ref_scores[fin], rtol=rtol, atol=1e-12)
+    np.testing.assert_allclose(scores[fin], ref_scores[fin], rtol=rtol, atol=atol)
     ndiff = 0
     for q in range(len(ids)):
         if np.array_equal(ids[q], ref_ids[q]):
@@ -51,8 +55,8 @@ def compare_topk(ids, scores, ref_ids, ref_scores, rtol=SCORE_RTOL):
             if ids[q, i] == ref_ids[q, i]:
                 continue
             # a swap is only allowed between candidates tied within rtol
-            assert abs(scores[q, i] - ref_scores[q, i]) <= rtol * abs(ref_scores[q, i]) + 1e-12
+            assert abs(scores[q, i] - ref_scores[q, i]) <= rtol * abs(ref_scores[q, i]) + atol
             if ids[q, i] not in ref_ids[q, :k]:
                 kth = ref_scores[q, k - 1]
-                assert abs(scores[q, i] - kth) <= rtol * abs(kth) + 1e-12, (q, i)
+                assert abs(scores[q, i] - kth) <= rtol * abs(kth) + atol, (q, i)
     return ndiff

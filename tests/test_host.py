@@ -39,7 +39,7 @@ def test_code_layout(lib):
     assert code_layout(200, 3, True) == (4, 8, 25)
     assert code_layout(200, 2, True) == (3, 10, 20)
     assert code_layout(64, 8, True) == (9, 3, 22)
-    assert code_layout(16, 4, False) == (4, 8, 2)
+    assert code_layout(16, 4, False) == (5, 6, 3)
 
 
 def test_host_double_to_half_matches_numpy(lib):
