@@ -351,7 +351,7 @@ def run_ours(args):
                                qrot.data_ptr(), 0, s))
     oid = torch.empty((nq, 10), dtype=torch.int64, device=dev)
     osc = torch.empty((nq, 10), dtype=torch.float64, device=dev)
-    sb = L.ivftq_scan_scratch_bytes(nq, n_p, 10)
+    sb = L.ivftq_scan_scratch_bytes(nq, n_p, 10, w.n_lists)
     sscr = torch.empty(sb, dtype=torch.uint8, device=dev)
     st = idx._store.struct()
 

@@ -149,11 +149,26 @@ int ivftq_probe(const double* qn, const float* centroids, int64_t nq, int n_list
 /* List scan + per-query top-`depth` (index.py:441-483): score =
  * coarse + (double)(||r|| * sum_j qrot_j * levels[code_j]). levels: f64
  * flattened reconstruction table (lloydmax.py:146-150). ids are internal. */
-size_t ivftq_scan_scratch_bytes(int64_t nq, int n_p, int depth);
+size_t ivftq_scan_scratch_bytes(int64_t nq, int n_p, int depth, int n_lists);
 int ivftq_scan_topk(const ivftq_store* store, const int32_t* probe, const double* coarse,
                     const float* qrot, const double* levels, int64_t nq, int n_p,
                     int depth, int64_t* ids_out, double* scores_out, void* scratch,
                     size_t scratch_bytes, void* stream);
+/* Query-major LUT scan (any bits, depth <= 7936): one CTA per (query, probe
+ * split) builds lut[j][c] = qrot_j * T[c] in shared memory. */
+int ivftq_scan_topk_lut(const ivftq_store* store, const int32_t* probe, const double* coarse,
+                        const float* qrot, const double* levels, int64_t nq, int n_p,
+                        int depth, int64_t* ids_out, double* scores_out, void* scratch,
+                        size_t scratch_bytes, void* stream);
+/* List-major tensor-core scan (bits 2..4, depth <= 32): probes regrouped by
+ * list; per (list, 128-query tile) the decoded codes meet the queries in
+ * tcgen05.mma (fp16 hi/lo error-compensated, fp32 accumulate in TMEM). */
+int ivftq_scan_tc_supported(int dim, int bits, int depth);
+size_t ivftq_scan_tc_scratch_bytes(int64_t nq, int n_p, int n_lists, int depth);
+int ivftq_scan_topk_tc(const ivftq_store* store, const int32_t* probe, const double* coarse,
+                       const float* qrot, const double* levels, int64_t nq, int n_p,
+                       int depth, int64_t* ids_out, double* scores_out, void* scratch,
+                       size_t scratch_bytes, void* stream);
 /* Exact re-score of the top-depth candidates against the raw f32 store and
  * re-order to top-k (index.py:470-473). */
 int ivftq_rerank(const float* raw, const double* qn, const int64_t* cand_ids,

@@ -70,9 +70,15 @@ _SIGS = {
     "ivftq_select_topn": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "ivftq_probe_scratch_bytes": (_sz, [_i64, _i32]),
     "ivftq_probe": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
-    "ivftq_scan_scratch_bytes": (_sz, [_i64, _i32, _i32]),
+    "ivftq_scan_scratch_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "ivftq_scan_topk": (_i32, [C.POINTER(IvftqStore), _vp, _vp, _vp, _vp, _i64, _i32, _i32,
                                _vp, _vp, _vp, _sz, _vp]),
+    "ivftq_scan_topk_lut": (_i32, [C.POINTER(IvftqStore), _vp, _vp, _vp, _vp, _i64, _i32, _i32,
+                                   _vp, _vp, _vp, _sz, _vp]),
+    "ivftq_scan_topk_tc": (_i32, [C.POINTER(IvftqStore), _vp, _vp, _vp, _vp, _i64, _i32, _i32,
+                                  _vp, _vp, _vp, _sz, _vp]),
+    "ivftq_scan_tc_supported": (_i32, [_i32, _i32, _i32]),
+    "ivftq_scan_tc_scratch_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "ivftq_rerank": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
     "ivftq_decode_scratch_bytes": (_sz, [_i64, _i32]),
     "ivftq_rowdot": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),

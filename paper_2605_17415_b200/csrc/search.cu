@@ -281,16 +281,33 @@ static int scan_splits(int64_t nq, int n_p) {
   return splits;
 }
 
-extern "C" size_t ivftq_scan_scratch_bytes(int64_t nq, int n_p, int depth) {
+static size_t lut_scratch_bytes(int64_t nq, int n_p, int depth) {
   int sp = scan_splits(nq, n_p);
   return (size_t)nq * sp * depth * (sizeof(double) + sizeof(int32_t)) + 512;
 }
 
-extern "C" int ivftq_scan_topk(const ivftq_store* st, const int32_t* probe,
-                               const double* coarse, const float* qrot, const double* levels,
-                               int64_t nq, int n_p, int depth, int64_t* ids_out,
-                               double* scores_out, void* scratch, size_t scratch_bytes,
-                               void* stream) {
+namespace ivftq {
+int merge_smem_opt_in(int K) {
+  return smem_opt_in((const void*)merge_kernel, BlockTopK::bytes(topk_cap(K, 128)));
+}
+void launch_merge(const double* part_s, const int32_t* part_id, int64_t nq, int n_in, int K,
+                  int64_t* ids_out, double* s_out, cudaStream_t s) {
+  merge_kernel<<<(unsigned)nq, 128, BlockTopK::bytes(topk_cap(K, 128)), s>>>(
+      part_s, part_id, n_in, K, ids_out, s_out);
+}
+}  // namespace ivftq
+
+extern "C" size_t ivftq_scan_scratch_bytes(int64_t nq, int n_p, int depth, int n_lists) {
+  size_t a = lut_scratch_bytes(nq, n_p, depth);
+  size_t b = ivftq_scan_tc_scratch_bytes(nq, n_p, n_lists, depth);
+  return a > b ? a : b;
+}
+
+extern "C" int ivftq_scan_topk_lut(const ivftq_store* st, const int32_t* probe,
+                                   const double* coarse, const float* qrot,
+                                   const double* levels, int64_t nq, int n_p, int depth,
+                                   int64_t* ids_out, double* scores_out, void* scratch,
+                                   size_t scratch_bytes, void* stream) {
   if (depth < 1 || depth > kMaxDepth) {
     set_error("scan_topk: depth %d outside [1, %d]", depth, kMaxDepth);
     return IVFTQ_ERR_UNSUPPORTED;
@@ -300,7 +317,7 @@ extern "C" int ivftq_scan_topk(const ivftq_store* st, const int32_t* probe,
     return IVFTQ_ERR_ARG;
   }
   if (nq == 0) return 0;
-  if (scratch_bytes < ivftq_scan_scratch_bytes(nq, n_p, depth)) {
+  if (scratch_bytes < lut_scratch_bytes(nq, n_p, depth)) {
     set_error("scan_topk: scratch too small");
     return IVFTQ_ERR_SCRATCH;
   }
@@ -331,7 +348,7 @@ extern "C" int ivftq_scan_topk(const ivftq_store* st, const int32_t* probe,
       LAUNCH(FB, false)            \
     }                              \
     break;
-    CASE(1) CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
+    CASE(2) CASE(3) CASE(4) CASE(5) CASE(6) CASE(7) CASE(8) CASE(9)
 #undef CASE
 #undef LAUNCH
     default:
@@ -339,11 +356,24 @@ extern "C" int ivftq_scan_topk(const ivftq_store* st, const int32_t* probe,
       return IVFTQ_ERR_UNSUPPORTED;
   }
   if (int e = check_launch("scan_lut")) return e;
-  size_t sm2 = BlockTopK::bytes(topk_cap(depth, 128));
-  if (int e = smem_opt_in((const void*)merge_kernel, sm2)) return e;
-  merge_kernel<<<(unsigned)nq, 128, sm2, s>>>(part_s, part_id, sp * depth, depth, ids_out,
-                                              scores_out);
+  if (int e = merge_smem_opt_in(depth)) return e;
+  launch_merge(part_s, part_id, nq, sp * depth, depth, ids_out, scores_out, s);
   return check_launch("merge");
+}
+
+// Batched queries with small depth go to the tensor-core list-major scan; a
+// handful of queries (few queries per probed list) or large depth use the
+// query-major LUT scan.
+extern "C" int ivftq_scan_topk(const ivftq_store* st, const int32_t* probe, const double* coarse,
+                               const float* qrot, const double* levels, int64_t nq, int n_p,
+                               int depth, int64_t* ids_out, double* scores_out, void* scratch,
+                               size_t scratch_bytes, void* stream) {
+  bool tc = nq >= 64 && ivftq_scan_tc_supported(st->dim, st->bits, depth);
+  if (tc)
+    return ivftq_scan_topk_tc(st, probe, coarse, qrot, levels, nq, n_p, depth, ids_out,
+                              scores_out, scratch, scratch_bytes, stream);
+  return ivftq_scan_topk_lut(st, probe, coarse, qrot, levels, nq, n_p, depth, ids_out,
+                             scores_out, scratch, scratch_bytes, stream);
 }
 
 extern "C" int ivftq_rerank(const float* raw, const double* qn, const int64_t* cand_ids,

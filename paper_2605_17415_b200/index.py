@@ -128,7 +128,13 @@ def _to_device_rows(x, dim_expected: int | None, dev, what="input"):
 
 
 class IvfTqIndex:
-    """Trained coarse partition over the fixed compression layer, on one GPU."""
+    """Trained coarse partition over the fixed compression layer, on one GPU.
+
+    `scan_mode` selects the list-scan kernel: "auto" (tensor-core list-major
+    scan for batches, LUT scan otherwise), "tc" or "lut".
+    """
+
+    scan_mode = "auto"
 
     def __init__(self, config: IndexConfig, quantizer: ScalarQuantizer, rot: RotationMatrix,
                  partition: CoarsePartition, device=None):
@@ -460,13 +466,13 @@ class IvfTqIndex:
                                            d, d, qrot.data_ptr(), _lib.IVFTQ_F32, s), "rotate")
         ids = torch.empty((max(nq, 1), depth), dtype=torch.int64, device=dev)
         scores = torch.empty((max(nq, 1), depth), dtype=torch.float64, device=dev)
-        sb = self._lib.ivftq_scan_scratch_bytes(nq, n_p, depth)
+        sb = self._lib.ivftq_scan_scratch_bytes(nq, n_p, depth, self.partition.n_lists)
         scr = torch.empty(sb, dtype=torch.uint8, device=dev)
-        _lib.check(self._lib.ivftq_scan_topk(C.byref(self._store.struct()), probe.data_ptr(),
-                                             coarse.data_ptr(), qrot.data_ptr(),
-                                             self._levels.data_ptr(), nq, n_p, depth,
-                                             ids.data_ptr(), scores.data_ptr(), scr.data_ptr(),
-                                             sb, s), "scan_topk")
+        fn = {"auto": self._lib.ivftq_scan_topk, "lut": self._lib.ivftq_scan_topk_lut,
+              "tc": self._lib.ivftq_scan_topk_tc}[self.scan_mode]
+        _lib.check(fn(C.byref(self._store.struct()), probe.data_ptr(), coarse.data_ptr(),
+                      qrot.data_ptr(), self._levels.data_ptr(), nq, n_p, depth, ids.data_ptr(),
+                      scores.data_ptr(), scr.data_ptr(), sb, s), "scan_topk")
         return ids, scores
 
     def _rerank(self, qn, nq, cand, depth, k):
