@@ -1,4 +1,4 @@
-// Tensor-core list scan (tcgen05) for batched search.
+// Tensor-core list scan (tcgen05) for batched search, warp-specialised.
 //
 // The reference scores every probed list with a per-list f32 GEMM,
 // w[members] @ q_rot[queries_of_list].T (index.py:442-458), then sorts all
@@ -6,22 +6,27 @@
 // structure on the 5th-gen tensor cores:
 //
 //   * probes are regrouped by list on the device (count / scan / scatter);
-//   * a work item is (list l, tile of <=128 queries probing l); persistent CTAs
-//     pull items from an atomic counter;
-//   * per NV-vector tile of l, one elected thread issues a 1-D TMA bulk copy of
-//     the packed codes + norms + ids (the 32-slot interleaved list layout makes
-//     a tile one contiguous span), prefetched one tile ahead;
-//   * all threads decode codes into fp16 operands in shared memory (UMMA
-//     K-major canonical layout) through a 2^(b+1)-entry level table, with the
-//     word/field walk unrolled per lcm(fields-per-word, 8) group;
-//   * one thread issues tcgen05.mma kind::f16 into a double-buffered TMEM
-//     accumulator, D[query][vector] = sum_j qrot_j * T[code_j];
-//   * epilogue: warp w reads TMEM lanes 32*(w%4).. (one query per thread) over
-//     its half of the tile's columns, filters candidates against the query's
-//     running k-th score, appends the few survivors to a per-thread shared
-//     buffer and drains it into a register top-K (the drain loop runs to the
-//     warp's max survivor count, so rare inserts stay cheap and convergent);
-//   * (query, list) winners go to a buffer merged per query afterwards.
+//     a work item is (list l, tile of <=128 queries probing l);
+//   * persistent CTAs, one per SM, run a four-role pipeline over the stream of
+//     NV-vector tiles of their items, handing off through mbarrier rings:
+//       - producer warp: pulls items from an atomic counter, writes the tile's
+//         control record + query rows into a stage slot, and one lane issues a
+//         1-D TMA bulk copy of the tile's packed codes, norms and ids (the
+//         32-slot interleaved list layout makes a tile one contiguous span);
+//       - 4 decoder warps: on an item's first tile build the A operand (the
+//         item's rotated queries, fp16 hi/lo) and, per tile, decode codes
+//         through a 2^(b+1)-entry level table into the B operand (UMMA K-major
+//         canonical layout, fp16 hi/lo), double-buffered;
+//       - MMA warp: one thread issues tcgen05.mma kind::f16 (3 products per
+//         K step, see below) into a double-buffered TMEM accumulator
+//         D[query][vector] and commits to the ring barriers;
+//       - 8 epilogue warps: warp w reads TMEM lanes 32*(w%4).. (one query per
+//         thread) over half of the tile's columns, filters candidates against
+//         the query's running k-th score, appends survivors to a per-thread
+//         shared buffer and drains it into a register top-K (the drain loop
+//         runs to the warp's max survivor count, so inserts stay convergent);
+//         at an item's last tile the two halves merge and (query, list)
+//         winners go to a buffer that a second kernel merges per query.
 //
 // Numerics: f32 values are split into fp16 hi + lo with power-of-two scaling
 // (T by 2^eT, q by 2^14) and D = Qhi.Thi + Qlo.Thi + Qhi.Tlo accumulated in
@@ -43,9 +48,16 @@ int merge_smem_opt_in(int K);
 
 namespace tc {
 
-constexpr int kThreads = 256;  // 8 warps: warp w and w+4 share TMEM lanes, split columns
-constexpr int kM = 128;        // queries per tile = MMA M
-constexpr int kDrain = 16;     // columns between candidate-buffer drains
+constexpr int kM = 128;          // queries per item = MMA M
+constexpr int kProdWarp = 0;     // producer (TMA + control records)
+constexpr int kMmaWarp = 1;      // tcgen05.mma issuer, owns TMEM
+constexpr int kDecWarp0 = 2;     // decoder warps 2..5
+constexpr int kDecWarps = 4;
+constexpr int kEpiWarp0 = 6;     // epilogue warps 6..13
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 448
+constexpr int kEpiThreads = 32 * kEpiWarps;
+constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
 
 struct Params {
   ivftq_store st;
@@ -59,41 +71,58 @@ struct Params {
   int32_t* counter;        // work counter (zeroed per launch)
   double* part_s;          // [nq*n_p*k]
   int32_t* part_id;
-  int n_p, k, d, DP, nbuf;
+  int n_p, k, d, DP, NV, NS;
   float t_scale;    // 2^eT
   float inv_scale;  // 2^-(eT+14)
 };
 
-struct Layout {
-  uint32_t qhi, qlo, bhi[2], blo[2], codes[2], norms[2], ids[2], nsc[2], vid[2], cand, tab,
-      bars, misc, total;
+// control record of one tile in a stage slot
+struct Ctrl {
+  int list;    // -1 = stop
+  int tile;    // tile index within the item
+  int ntiles;
+  int valid;   // vectors of this tile that exist
+  int nqt;     // queries in the item
+  int pad[3];
 };
 
-__host__ __device__ inline Layout make_layout(int NV, int nbuf, int DP, int W, int C) {
+struct Layout {
+  uint32_t qhi, qlo, bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
+      st_qrow, cand, tab, bars, misc, total;
+};
+
+__host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) & ~(a - 1); }
+
+// candidate-buffer entries per epilogue thread: a drain window, or a whole
+// top-K list when the two column halves merge
+__host__ __device__ inline int cand_entries(int kmax) { return kmax > kDrain ? kmax : kDrain; }
+
+__host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int C, int KMAX) {
   Layout L{};
   uint32_t off = 0;
   auto take = [&](uint32_t bytes) {
     uint32_t o = off;
-    off = (off + bytes + 127u) & ~127u;
+    off = align_up(off + bytes, 128u);
     return o;
   };
   L.qhi = take(kM * DP * 2);
   L.qlo = take(kM * DP * 2);
   for (int b = 0; b < 2; ++b) {
-    L.bhi[b] = b < nbuf ? take(NV * DP * 2) : L.bhi[0];
-    L.blo[b] = b < nbuf ? take(NV * DP * 2) : L.blo[0];
+    L.bhi[b] = take(NV * DP * 2);
+    L.blo[b] = take(NV * DP * 2);
   }
-  for (int b = 0; b < 2; ++b) {
-    L.codes[b] = take(NV * W * 4);
-    L.norms[b] = take(NV * 2);
-    L.ids[b] = take(NV * 4);
-    L.nsc[b] = take(NV * 4);
-    L.vid[b] = take(NV * 4);
-  }
-  L.cand = take(kDrain * kThreads * 8);
+  // stage slot: codes | norms | ids | ctrl | qrow  (each 128-aligned)
+  L.st_codes = 0;
+  L.st_norms = align_up(NV * (uint32_t)W * 4, 128);
+  L.st_ids = L.st_norms + align_up(NV * 2, 128);
+  L.st_ctrl = L.st_ids + align_up(NV * 4, 128);
+  L.st_qrow = L.st_ctrl + 128;
+  L.stage_bytes = L.st_qrow + kM * 4;
+  L.stage = take(L.stage_bytes * NS);
+  L.cand = take(cand_entries(KMAX) * kEpiThreads * 8);
   L.tab = take(C * 4);
-  L.bars = take(64);
-  L.misc = take(kM * 4 + 64);
+  L.bars = take(8 * (2 * 8 + 10));
+  L.misc = take(64);
   L.total = off;
   return L;
 }
@@ -133,12 +162,28 @@ struct RegTopK {
   }
 };
 
-#define SEL(arr, b) ((b) ? (arr)[1] : (arr)[0])
-
 constexpr int gcd_c(int a, int b) { return b ? gcd_c(b, a % b) : a; }
 
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(sm100::smem_u32(bar)) : "memory");
+}
+// 32 lanes x 16 consecutive 32-bit TMEM columns
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+}
+
 template <int FB, int KMAX>
-__global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P, int NV) {
+__global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   constexpr int C = 1 << FB;
   constexpr int FPW = 32 / FB;
   constexpr uint32_t MASK = (1u << FB) - 1u;
@@ -146,19 +191,22 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P, int NV) 
   constexpr int GW = G / FPW, GC = G / 8;     // words, 8-field chunks per group
   extern __shared__ __align__(1024) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NV = P.NV, NS = P.NS;
   const int W = P.st.words_per_vec, DP = P.DP, d = P.d, NCH = DP / 8;
-  const int NG = (DP + G - 1) / G;
-  const int nbuf = P.nbuf;
-  const uint32_t tmem_cols = 2 * NV < 32 ? 32 : 2 * NV;
-  const Layout Lo = make_layout(NV, nbuf, DP, W, C);
+  const uint32_t tmem_cols = 2 * NV < 32 ? 32u : (2 * NV <= 64 ? 64u : (2 * NV <= 128 ? 128u : 256u));
+  const Layout Lo = make_layout(NV, NS, DP, W, C, KMAX);
   uint32_t* tab = (uint32_t*)(smem + Lo.tab);
-  uint64_t* load_bar = (uint64_t*)(smem + Lo.bars);
-  uint64_t* mma_bar = load_bar + 2;
+  uint64_t* bars = (uint64_t*)(smem + Lo.bars);
+  uint64_t* st_full = bars;            // [NS] producer -> decoders/epilogue (TMA tx)
+  uint64_t* st_empty = bars + 8;       // [NS] decoders + epilogue -> producer
+  uint64_t* op_full = bars + 16;       // [2] decoders -> MMA
+  uint64_t* op_empty = bars + 18;      // [2] MMA commit -> decoders
+  uint64_t* acc_full = bars + 20;      // [2] MMA commit -> epilogue
+  uint64_t* acc_empty = bars + 22;     // [2] epilogue -> MMA
+  uint64_t* a_full = bars + 24;        // decoders -> MMA (A operand built)
+  uint64_t* a_empty = bars + 25;       // MMA commit -> decoders (A operand free)
   uint32_t* tmem_slot = (uint32_t*)(smem + Lo.misc);
-  int* bcast = (int*)(smem + Lo.misc + 16);
-  int* qrow = (int*)(smem + Lo.misc + 64);  // pair flat index per query row
-  float* cand_v = (float*)(smem + Lo.cand);
-  int* cand_c = (int*)(smem + Lo.cand + kDrain * kThreads * 4);
+  auto stage = [&](int s) { return smem + Lo.stage + (uint32_t)s * Lo.stage_bytes; };
 
   // ---- one-time setup ---------------------------------------------------------
   for (int c = tid; c < C; c += kThreads) {
@@ -166,12 +214,20 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P, int NV) 
     uint32_t hi = split_pack((float)P.levels[c] * P.t_scale, lo);
     tab[c] = hi | (lo << 16);
   }
-  if (warp == 0) sm100::tmem_alloc(tmem_slot, tmem_cols);
+  if (warp == kMmaWarp) sm100::tmem_alloc(tmem_slot, tmem_cols);
   if (tid == 0) {
-    sm100::mbar_init(&load_bar[0], 1);
-    sm100::mbar_init(&load_bar[1], 1);
-    sm100::mbar_init(&mma_bar[0], 1);
-    sm100::mbar_init(&mma_bar[1], 1);
+    for (int s = 0; s < NS; ++s) {
+      sm100::mbar_init(&st_full[s], 1);
+      sm100::mbar_init(&st_empty[s], kDecWarps + kEpiWarps);
+    }
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&op_full[b], kDecWarps);
+      sm100::mbar_init(&op_empty[b], 1);
+      sm100::mbar_init(&acc_full[b], 1);
+      sm100::mbar_init(&acc_empty[b], kEpiWarps);
+    }
+    sm100::mbar_init(a_full, kDecWarps);
+    sm100::mbar_init(a_empty, 1);
     sm100::mbar_fence_init();
   }
   sm100::fence_proxy_async_smem();
@@ -179,161 +235,91 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P, int NV) 
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t idesc = sm100::idesc_f16_f32(kM, NV);
-  const uint32_t a_lbo = kM * 16, b_lbo = NV * 16, sbo = 128;
-  const uint32_t qhi_a = sm100::smem_u32(smem + Lo.qhi), qlo_a = sm100::smem_u32(smem + Lo.qlo);
-  const int n_items = *P.n_items;
-  const int row = (warp & 3) * 32 + lane;  // query row == TMEM lane
-  const int half = warp >> 2;              // which half of each tile's columns
-  uint32_t g = 0;  // tiles processed by this CTA
 
-  for (;;) {
-    if (tid == 0) bcast[0] = atomicAdd(P.counter, 1);
-    __syncthreads();
-    const int item = bcast[0];
-    if (item >= n_items) break;
-    const int2 it = P.items[item];
-    const int l = it.x;
-    const int pbase = P.pstart[l] + it.y * kM;
-    const int nqt = min(kM, P.pstart[l + 1] - pbase);
-    if (tid < kM) qrow[tid] = tid < nqt ? P.pair_idx[pbase + tid] : -1;
-    const int size = P.st.list_size[l];
-    const int64_t off = P.st.list_offset[l];
-    const int ntiles = (size + NV - 1) / NV;
-
-    auto issue_load = [&](int tile, uint32_t sb) {
-      int64_t s0 = off + (int64_t)tile * NV;
-      uint32_t cb = NV * W * 4, nb = NV * 2, ib = NV * 4;
-      sm100::mbar_arrive_expect_tx(&load_bar[sb], cb + nb + ib);
-      sm100::bulk_g2s(smem + SEL(Lo.codes, sb), P.st.codes + (s0 >> 5) * W * 32, cb, &load_bar[sb]);
-      sm100::bulk_g2s(smem + SEL(Lo.norms, sb), P.st.norms + s0, nb, &load_bar[sb]);
-      sm100::bulk_g2s(smem + SEL(Lo.ids, sb), P.st.ids + s0, ib, &load_bar[sb]);
-    };
-    if (tid == 0 && ntiles > 0) issue_load(0, g & 1);
-    __syncthreads();
-
-    // ---- A operand: this tile's rotated queries, split hi/lo, scaled 2^14 ------
-    for (int task = tid; task < kM * NCH; task += kThreads) {
-      int r = task % kM, c = task / kM;
-      int pi = qrow[r];
-      uint32_t h[8], lw[8];
-      const float* qv = pi >= 0 ? P.qrot + (int64_t)(pi / P.n_p) * d : nullptr;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        int j = c * 8 + e;
-        float x = (qv && j < d) ? __ldg(qv + j) * 16384.0f : 0.0f;
-        h[e] = split_pack(x, lw[e]);
+  if (warp == kProdWarp) {
+    // ================= producer =================================================
+    const int n_items = *P.n_items;
+    uint32_t t = 0;
+    for (;;) {
+      int item = 0;
+      if (lane == 0) item = atomicAdd(P.counter, 1);
+      item = __shfl_sync(kFull, item, 0);
+      if (item >= n_items) {
+        const int s = t % NS;
+        if (t >= (uint32_t)NS) sm100::mbar_wait(&st_empty[s], ((t / NS) - 1) & 1);
+        if (lane == 0) {
+          Ctrl* c = (Ctrl*)(stage(s) + Lo.st_ctrl);
+          c->list = -1;
+          mbar_arrive(&st_full[s]);
+        }
+        break;
       }
-      uint4 vh = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16),
-                            h[6] | (h[7] << 16));
-      uint4 vl = make_uint4(lw[0] | (lw[1] << 16), lw[2] | (lw[3] << 16),
-                            lw[4] | (lw[5] << 16), lw[6] | (lw[7] << 16));
-      uint32_t o = c * (kM * 16) + (r >> 3) * 128 + (r & 7) * 16;
-      *(uint4*)(smem + Lo.qhi + o) = vh;
-      *(uint4*)(smem + Lo.qlo + o) = vl;
+      const int2 it = P.items[item];
+      const int l = it.x;
+      const int pbase = P.pstart[l] + it.y * kM;
+      const int nqt = min(kM, P.pstart[l + 1] - pbase);
+      const int size = P.st.list_size[l];
+      const int64_t off = P.st.list_offset[l];
+      const int ntiles = (size + NV - 1) / NV;
+      if (ntiles == 0) {  // empty list: every probing query gets -inf padding
+        for (int r = lane; r < nqt; r += 32) {
+          const int64_t ob = (int64_t)P.pair_idx[pbase + r] * P.k;
+          for (int p = 0; p < P.k; ++p) {
+            P.part_s[ob + p] = -INFINITY;
+            P.part_id[ob + p] = INT_MAX;
+          }
+        }
+        continue;
+      }
+      for (int i = 0; i < ntiles; ++i, ++t) {
+        const int s = t % NS;
+        if (t >= (uint32_t)NS) sm100::mbar_wait(&st_empty[s], ((t / NS) - 1) & 1);
+        unsigned char* sp = stage(s);
+        int* qrow = (int*)(sp + Lo.st_qrow);
+        for (int r = lane; r < kM; r += 32) qrow[r] = r < nqt ? P.pair_idx[pbase + r] : -1;
+        if (lane == 0) {
+          Ctrl* c = (Ctrl*)(sp + Lo.st_ctrl);
+          c->list = l;
+          c->tile = i;
+          c->ntiles = ntiles;
+          c->valid = min(NV, size - i * NV);
+          c->nqt = nqt;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          const int64_t s0 = off + (int64_t)i * NV;
+          const uint32_t cb = NV * W * 4, nb = NV * 2, ib = NV * 4;
+          sm100::mbar_arrive_expect_tx(&st_full[s], cb + nb + ib);
+          sm100::bulk_g2s(sp + Lo.st_codes, P.st.codes + (s0 >> 5) * W * 32, cb, &st_full[s]);
+          sm100::bulk_g2s(sp + Lo.st_norms, P.st.norms + s0, nb, &st_full[s]);
+          sm100::bulk_g2s(sp + Lo.st_ids, P.st.ids + s0, ib, &st_full[s]);
+        }
+      }
     }
-
-    RegTopK<KMAX> top;
-    top.init();
-
-    auto epilogue = [&](uint32_t gt) {
-      const uint32_t ab = gt & 1;
-      sm100::mbar_wait(&mma_bar[ab], (gt >> 1) & 1);
+  } else if (warp == kMmaWarp) {
+    // ================= MMA issuer ===============================================
+    const uint32_t idesc = sm100::idesc_f16_f32(kM, NV);
+    const uint32_t a_lbo = kM * 16, b_lbo = NV * 16, sbo = 128;
+    const uint32_t qhi_a = sm100::smem_u32(smem + Lo.qhi), qlo_a = sm100::smem_u32(smem + Lo.qlo);
+    uint32_t t = 0, u = 0;
+    for (;;) {
+      const int ob = t & 1;
+      sm100::mbar_wait(&op_full[ob], (t >> 1) & 1);
+      const Ctrl c = *(const Ctrl*)(stage(t % NS) + Lo.st_ctrl);
+      if (t >= 2) sm100::mbar_wait(&acc_empty[ob], ((t >> 1) - 1) & 1);
+      if (c.list < 0) {
+        if (lane == 0) mbar_arrive(&acc_full[ob]);
+        break;
+      }
+      if (c.tile == 0) {
+        sm100::mbar_wait(a_full, u & 1);
+        ++u;
+      }
       sm100::tc_fence_after();
-      const float* nsc = (const float*)(smem + SEL(Lo.nsc, ab));
-      const int* vid = (const int*)(smem + SEL(Lo.vid, ab));
-      const int c0 = half * (NV / 2);
-#pragma unroll 1
-      for (int cc = 0; cc < NV / 2; cc += 32) {
-        uint32_t r[32];
-        sm100::tmem_ld32(tmem + ((uint32_t)((warp & 3) * 32) << 16) + ab * NV + c0 + cc, r);
-        sm100::tmem_ld_wait();
-#pragma unroll
-        for (int h2 = 0; h2 < 32; h2 += kDrain) {
-          int cnt = 0;
-          const float thr = top.s[KMAX - 1];
-#pragma unroll
-          for (int e = 0; e < kDrain; ++e) {
-            const int col = c0 + cc + h2 + e;
-            float res = __fmul_rn(__uint_as_float(r[h2 + e]), nsc[col]);
-            if (res >= thr) {
-              cand_v[cnt * kThreads + tid] = res;
-              cand_c[cnt * kThreads + tid] = col;
-              ++cnt;
-            }
-          }
-          const int mx = __reduce_max_sync(kFull, cnt);
-          for (int i = 0; i < mx; ++i) {
-            if (i < cnt) {
-              float v = cand_v[i * kThreads + tid];
-              int id = vid[cand_c[i * kThreads + tid]];
-              if (top.beats(v, id)) top.insert(v, id);
-            }
-          }
-        }
-      }
-      sm100::tc_fence_before();
-    };
-
-    for (int i = 0; i < ntiles; ++i) {
-      const uint32_t gt = g + i;
-      const uint32_t sb = gt & 1;                       // stage + accumulator buffer
-      const uint32_t bb = nbuf == 2 ? (gt & 1) : 0;     // operand buffer
-      __syncthreads();  // readers of this iteration's buffers are done
-      if (tid == 0 && i + 1 < ntiles) issue_load(i + 1, sb ^ 1);
-      sm100::mbar_wait(&load_bar[sb], (gt >> 1) & 1);
-      // ---- decode tile i: codes -> fp16 hi/lo operand rows ------------------
-      const uint32_t* cw = (const uint32_t*)(smem + SEL(Lo.codes, sb));
-      for (int task = tid; task < NV * NG; task += kThreads) {
-        const int v = task % NV, gi = task / NV;
-        const uint32_t* wv = cw + (v >> 5) * W * 32 + (v & 31);
-        uint32_t words[GW];
-#pragma unroll
-        for (int u = 0; u < GW; ++u) {
-          int w = gi * GW + u;
-          words[u] = w < W ? wv[w * 32] : 0u;
-        }
-#pragma unroll
-        for (int cc = 0; cc < GC; ++cc) {
-          const int c = gi * GC + cc;
-          if (c < NCH) {
-            uint32_t hi[8], lo[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int f = cc * 8 + e;  // field within group (compile time)
-              uint32_t t = tab[(words[f / FPW] >> ((f % FPW) * FB)) & MASK];
-              hi[e] = t & 0xFFFFu;
-              lo[e] = t >> 16;
-            }
-            uint4 vh = make_uint4(hi[0] | (hi[1] << 16), hi[2] | (hi[3] << 16),
-                                  hi[4] | (hi[5] << 16), hi[6] | (hi[7] << 16));
-            uint4 vl = make_uint4(lo[0] | (lo[1] << 16), lo[2] | (lo[3] << 16),
-                                  lo[4] | (lo[5] << 16), lo[6] | (lo[7] << 16));
-            uint32_t o = c * (NV * 16) + (v >> 3) * 128 + (v & 7) * 16;
-            *(uint4*)(smem + SEL(Lo.bhi, bb) + o) = vh;
-            *(uint4*)(smem + SEL(Lo.blo, bb) + o) = vl;
-          }
-        }
-      }
-      {
-        const int valid = min(NV, size - i * NV);
-        const uint16_t* nb = (const uint16_t*)(smem + SEL(Lo.norms, sb));
-        const int* ib = (const int*)(smem + SEL(Lo.ids, sb));
-        float* nsc = (float*)(smem + SEL(Lo.nsc, sb));
-        int* vid = (int*)(smem + SEL(Lo.vid, sb));
-        for (int v = tid; v < NV; v += kThreads) {
-          nsc[v] = v < valid ? h2f_bits(nb[v]) * P.inv_scale : __int_as_float(0x7fc00000);
-          vid[v] = v < valid ? ib[v] : INT_MAX;
-        }
-      }
-      sm100::fence_proxy_async_smem();
-      sm100::tc_fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        sm100::tc_fence_after();
-        const uint32_t bh = sm100::smem_u32(smem + SEL(Lo.bhi, bb));
-        const uint32_t bl = sm100::smem_u32(smem + SEL(Lo.blo, bb));
-        const uint32_t dt = tmem + sb * NV;
+      if (lane == 0) {
+        const uint32_t bh = sm100::smem_u32(smem + (ob ? Lo.bhi[1] : Lo.bhi[0]));
+        const uint32_t bl = sm100::smem_u32(smem + (ob ? Lo.blo[1] : Lo.blo[0]));
+        const uint32_t dt = tmem + ob * NV;
         const int ks = DP / 16;
         uint32_t acc = 0;
         for (int pass = 0; pass < 3; ++pass) {
@@ -346,49 +332,193 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P, int NV) 
             acc = 1;
           }
         }
-        sm100::mma_commit(&mma_bar[sb]);
+        sm100::mma_commit(&op_empty[ob]);
+        sm100::mma_commit(&acc_full[ob]);
+        if (c.tile == c.ntiles - 1) sm100::mma_commit(a_empty);
       }
-      if (nbuf == 2) {
-        if (i > 0) epilogue(gt - 1);
-      } else {
-        epilogue(gt);
-      }
+      __syncwarp();
+      ++t;
     }
-    if (nbuf == 2 && ntiles > 0) epilogue(g + ntiles - 1);
-    g += ntiles;
-
-    // ---- combine the two column halves, write (query, list) winners -----------
-    __syncthreads();
-    if (half == 1) {
-#pragma unroll
-      for (int p = 0; p < KMAX; ++p) {
-        cand_v[p * kM + row] = top.s[p];
-        cand_c[p * kM + row] = top.i[p];
+  } else if (warp < kEpiWarp0) {
+    // ================= decoders (+ A operand builders) =========================
+    const int dt_ = tid - 32 * kDecWarp0;  // 0..127
+    constexpr int kDecThreads = 32 * kDecWarps;
+    const int NG = (DP + G - 1) / G;
+    uint32_t t = 0, u = 0;
+    for (;;) {
+      const int s = t % NS;
+      sm100::mbar_wait(&st_full[s], (t / NS) & 1);
+      unsigned char* sp = stage(s);
+      const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
+      const int ob = t & 1;
+      if (t >= 2) sm100::mbar_wait(&op_empty[ob], ((t >> 1) - 1) & 1);
+      if (c.list < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&op_full[ob]);
+        break;
       }
-    }
-    __syncthreads();
-    if (half == 0 && row < nqt) {
-#pragma unroll 1
-      for (int p = 0; p < KMAX; ++p) {
-        float v = cand_v[p * kM + row];
-        int id = cand_c[p * kM + row];
-        if (id != INT_MAX && top.beats(v, id)) top.insert(v, id);
-      }
-      const int pi = qrow[row];
-      const double cs = P.coarse[pi];
-      const int64_t ob = (int64_t)pi * P.k;
+      if (c.tile == 0) {
+        // A operand for the new item: wait until the previous item's MMAs are done
+        if (u > 0) sm100::mbar_wait(a_empty, (u - 1) & 1);
+        const int* qrow = (const int*)(sp + Lo.st_qrow);
+        for (int task = dt_; task < kM * NCH; task += kDecThreads) {
+          const int r = task % kM, ch = task / kM;
+          const int pi = qrow[r];
+          uint32_t h[8], lw[8];
+          const float* qv = pi >= 0 ? P.qrot + (int64_t)(pi / P.n_p) * d : nullptr;
 #pragma unroll
-      for (int p = 0; p < KMAX; ++p) {
-        if (p < P.k) {
-          bool have = top.i[p] != INT_MAX;
-          P.part_s[ob + p] = have ? cs + (double)top.s[p] : -INFINITY;
-          P.part_id[ob + p] = have ? top.i[p] : INT_MAX;
+          for (int e = 0; e < 8; ++e) {
+            const int j = ch * 8 + e;
+            const float x = (qv && j < d) ? __ldg(qv + j) * 16384.0f : 0.0f;
+            h[e] = split_pack(x, lw[e]);
+          }
+          const uint32_t o = ch * (kM * 16) + (r >> 3) * 128 + (r & 7) * 16;
+          *(uint4*)(smem + Lo.qhi + o) = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16),
+                                                    h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+          *(uint4*)(smem + Lo.qlo + o) =
+              make_uint4(lw[0] | (lw[1] << 16), lw[2] | (lw[3] << 16), lw[4] | (lw[5] << 16),
+                         lw[6] | (lw[7] << 16));
+        }
+        sm100::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full);
+        ++u;
+      }
+      // ---- decode this tile's codes into the B operand ----------------------------
+      const uint32_t* cw = (const uint32_t*)(sp + Lo.st_codes);
+      unsigned char* bhi = smem + (ob ? Lo.bhi[1] : Lo.bhi[0]);
+      unsigned char* blo = smem + (ob ? Lo.blo[1] : Lo.blo[0]);
+      const int nvshift = __ffs(NV) - 1;
+      for (int task = dt_; task < NV * NG; task += kDecThreads) {
+        const int v = task & (NV - 1), gi = task >> nvshift;
+        const uint32_t* wv = cw + (v >> 5) * W * 32 + (v & 31);
+        uint32_t words[GW];
+#pragma unroll
+        for (int q = 0; q < GW; ++q) {
+          const int w = gi * GW + q;
+          words[q] = w < W ? wv[w * 32] : 0u;
+        }
+#pragma unroll
+        for (int cc = 0; cc < GC; ++cc) {
+          const int ch = gi * GC + cc;
+          if (ch < NCH) {
+            uint32_t hi[8], lo[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int f = cc * 8 + e;  // field within group (compile time)
+              const uint32_t tv = tab[(words[f / FPW] >> ((f % FPW) * FB)) & MASK];
+              hi[e] = tv & 0xFFFFu;
+              lo[e] = tv >> 16;
+            }
+            const uint32_t o = ch * (NV * 16) + (v >> 3) * 128 + (v & 7) * 16;
+            *(uint4*)(bhi + o) = make_uint4(hi[0] | (hi[1] << 16), hi[2] | (hi[3] << 16),
+                                            hi[4] | (hi[5] << 16), hi[6] | (hi[7] << 16));
+            *(uint4*)(blo + o) = make_uint4(lo[0] | (lo[1] << 16), lo[2] | (lo[3] << 16),
+                                            lo[4] | (lo[5] << 16), lo[6] | (lo[7] << 16));
+          }
         }
       }
+      sm100::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&op_full[ob]);
+        mbar_arrive(&st_empty[s]);
+      }
+      ++t;
+    }
+  } else {
+    // ================= epilogue =================================================
+    const int et = tid - 32 * kEpiWarp0;   // 0..255
+    const int quad = warp & 3;             // TMEM lane quadrant (warp_id % 4)
+    const int half = (warp - kEpiWarp0) >> 2;
+    const int row = quad * 32 + lane;      // query row == TMEM lane
+    float* cand_v = (float*)(smem + Lo.cand);
+    int* cand_c = (int*)(smem + Lo.cand + cand_entries(KMAX) * kEpiThreads * 4);
+    RegTopK<KMAX> top;
+    top.init();
+    uint32_t t = 0;
+    const int cols = NV / 2;
+    for (;;) {
+      const int ab = t & 1, s = t % NS;
+      sm100::mbar_wait(&acc_full[ab], (t >> 1) & 1);
+      sm100::mbar_wait(&st_full[s], (t / NS) & 1);
+      unsigned char* sp = stage(s);
+      const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
+      if (c.list < 0) break;
+      if (c.tile == 0) top.init();
+      sm100::tc_fence_after();
+      const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
+      const int* ids = (const int*)(sp + Lo.st_ids);
+      const int c0 = half * cols;
+#pragma unroll 1
+      for (int cc = 0; cc < cols; cc += kDrain) {
+        uint32_t r[kDrain];
+        tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
+        sm100::tmem_ld_wait();
+        const float thr = top.s[KMAX - 1];
+        int cnt = 0;
+#pragma unroll
+        for (int e = 0; e < kDrain; ++e) {
+          const int col = c0 + cc + e;
+          const float nsc = col < c.valid ? h2f_bits(nrm[col]) * P.inv_scale
+                                          : __int_as_float(0x7fc00000);
+          const float res = __fmul_rn(__uint_as_float(r[e]), nsc);
+          if (res >= thr) {
+            cand_v[cnt * kEpiThreads + et] = res;
+            cand_c[cnt * kEpiThreads + et] = col;
+            ++cnt;
+          }
+        }
+        const int mx = __reduce_max_sync(kFull, cnt);
+        for (int i = 0; i < mx; ++i) {
+          if (i < cnt) {
+            const float v = cand_v[i * kEpiThreads + et];
+            const int id = ids[cand_c[i * kEpiThreads + et]];
+            if (top.beats(v, id)) top.insert(v, id);
+          }
+        }
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      if (c.tile == c.ntiles - 1) {
+        // merge the column halves of each query row, then emit (query, list) winners
+        if (half == 1) {
+#pragma unroll
+          for (int p = 0; p < KMAX; ++p) {
+            cand_v[p * kEpiThreads + et] = top.s[p];
+            cand_c[p * kEpiThreads + et] = top.i[p];
+          }
+        }
+        named_bar(1, kEpiThreads);
+        if (half == 0 && row < c.nqt) {
+#pragma unroll 1
+          for (int p = 0; p < KMAX; ++p) {
+            const float v = cand_v[p * kEpiThreads + et + 128];
+            const int id = cand_c[p * kEpiThreads + et + 128];
+            if (id != INT_MAX && top.beats(v, id)) top.insert(v, id);
+          }
+          const int pi = ((const int*)(sp + Lo.st_qrow))[row];
+          const double cs = P.coarse[pi];
+          const int64_t o = (int64_t)pi * P.k;
+#pragma unroll
+          for (int p = 0; p < KMAX; ++p) {
+            if (p < P.k) {
+              const bool have = top.i[p] != INT_MAX;
+              P.part_s[o + p] = have ? cs + (double)top.s[p] : -INFINITY;
+              P.part_id[o + p] = have ? top.i[p] : INT_MAX;
+            }
+          }
+        }
+        named_bar(1, kEpiThreads);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&st_empty[s]);
+      ++t;
     }
   }
   __syncthreads();
-  if (warp == 0) sm100::tmem_dealloc(tmem, tmem_cols);
+  if (warp == kMmaWarp) sm100::tmem_dealloc(tmem, tmem_cols);
 }
 
 // ---- probe regrouping: pairs (q, p) bucketed by list ---------------------------
@@ -504,13 +634,15 @@ extern "C" size_t ivftq_scan_tc_scratch_bytes(int64_t nq, int n_p, int n_lists, 
 
 static const size_t kSmemLimit = 227 * 1024;
 
-// Largest vector tile (double-buffered operands first) that fits in shared memory.
-static bool pick_tile(int DP, int W, int C, int* nv, int* nbuf) {
-  const int cands[4][2] = {{128, 2}, {64, 2}, {64, 1}, {32, 1}};
+// Widest vector tile, then deepest stage ring, that fits in shared memory.
+static int kmax_for(int depth) { return depth <= 10 ? 10 : 32; }
+
+static bool pick_tile(int DP, int W, int C, int kmax, int* nv, int* ns) {
+  const int cands[6][2] = {{128, 4}, {128, 3}, {64, 4}, {64, 3}, {32, 4}, {32, 3}};
   for (auto& c : cands) {
-    if (make_layout(c[0], c[1], DP, W, C).total + 1024 <= kSmemLimit) {
+    if (make_layout(c[0], c[1], DP, W, C, kmax).total + 1024 <= kSmemLimit) {
       *nv = c[0];
-      *nbuf = c[1];
+      *ns = c[1];
       return true;
     }
   }
@@ -522,12 +654,12 @@ extern "C" int ivftq_scan_tc_supported(int dim, int bits, int depth) {
   if (fb < 3 || fb > 5 || depth < 1 || depth > 32) return 0;
   int DP = (dim + 15) / 16 * 16;
   int W = words_per_vec(dim, fb);
-  int nv, nbuf;
-  return pick_tile(DP, W, 1 << fb, &nv, &nbuf) && nv >= 64;
+  int nv, ns;
+  return pick_tile(DP, W, 1 << fb, kmax_for(depth), &nv, &ns);
 }
 
 template <int FB, int KMAX>
-static int launch_tc(const Params& P, int NV, size_t smem, int grid, cudaStream_t s) {
+static int launch_tc(const Params& P, size_t smem, int grid, cudaStream_t s) {
   auto fn = scan_tc_kernel<FB, KMAX>;
   cudaError_t e = cudaFuncSetAttribute((const void*)fn,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -535,7 +667,7 @@ static int launch_tc(const Params& P, int NV, size_t smem, int grid, cudaStream_
     set_error("scan_tc: smem %zu rejected: %s", smem, cudaGetErrorString(e));
     return IVFTQ_ERR_UNSUPPORTED;
   }
-  fn<<<grid, kThreads, smem, s>>>(P, NV);
+  fn<<<grid, kThreads, smem, s>>>(P);
   return check_launch("scan_tc");
 }
 
@@ -575,9 +707,9 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
 
   const int fb = st->field_bits, C = 1 << fb;
   const int DP = (st->dim + 15) / 16 * 16;
-  int NV = 0, nbuf = 0;
-  pick_tile(DP, st->words_per_vec, C, &NV, &nbuf);
   Params P{};
+  const int kmax = kmax_for(depth);
+  pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS);
   P.st = *st;
   P.coarse = coarse;
   P.qrot = qrot;
@@ -593,19 +725,18 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   P.k = depth;
   P.d = st->dim;
   P.DP = DP;
-  P.nbuf = nbuf;
   // Every Lloyd-Max level satisfies |T| < 5/sqrt(d) < 4, so 2^12 keeps the
   // scaled table below 2^14 and its hi/lo halves in the fp16 normal range.
   const int eT = 12;
   P.t_scale = ldexpf(1.0f, eT);
   P.inv_scale = ldexpf(1.0f, -(eT + 14));
-  size_t smem = make_layout(NV, nbuf, DP, st->words_per_vec, C).total + 1024;
+  size_t smem = make_layout(P.NV, P.NS, DP, st->words_per_vec, C, kmax).total + 1024;
   int grid = g_num_sms;
   int rc;
 #define TC_CASE(FBV)                                                              \
   if (fb == FBV) {                                                                \
-    rc = depth <= 10 ? launch_tc<FBV, 10>(P, NV, smem, grid, s)                   \
-                     : launch_tc<FBV, 32>(P, NV, smem, grid, s);                  \
+    rc = kmax == 10 ? launch_tc<FBV, 10>(P, smem, grid, s)                        \
+                    : launch_tc<FBV, 32>(P, smem, grid, s);                       \
   }
   TC_CASE(3) else TC_CASE(4) else TC_CASE(5) else {
     set_error("scan_tc: field width %d", fb);
