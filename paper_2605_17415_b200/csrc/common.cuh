@@ -68,6 +68,9 @@ IVFTQ_HD uint16_t d2h_bits(double x) {
 }
 
 IVFTQ_HD float h2f_bits(uint16_t h) {
+#ifdef __CUDA_ARCH__
+  return __half2float(__ushort_as_half(h));  // exact, one conversion instruction
+#endif
   uint32_t s = (uint32_t)(h & 0x8000u) << 16;
   uint32_t e = (h >> 10) & 0x1f;
   uint32_t m = h & 0x3ff;

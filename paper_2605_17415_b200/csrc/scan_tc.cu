@@ -58,6 +58,7 @@ constexpr int kEpiWarps = 8;
 constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 448
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
+constexpr int kNS = 4;           // stage ring depth (power of two)
 
 struct Params {
   ivftq_store st;
@@ -88,7 +89,7 @@ struct Ctrl {
 
 struct Layout {
   uint32_t qhi, qlo, bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
-      st_qrow, cand, tab, bars, misc, total;
+      st_qrow, st_nsc, cand, tab, bars, misc, total;
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) & ~(a - 1); }
@@ -117,7 +118,8 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.st_ids = L.st_norms + align_up(NV * 2, 128);
   L.st_ctrl = L.st_ids + align_up(NV * 4, 128);
   L.st_qrow = L.st_ctrl + 128;
-  L.stage_bytes = L.st_qrow + kM * 4;
+  L.st_nsc = L.st_qrow + kM * 4;
+  L.stage_bytes = L.st_nsc + align_up(NV * 4, 128);
   L.stage = take(L.stage_bytes * NS);
   L.cand = take(cand_entries(KMAX) * kEpiThreads * 8);
   L.tab = take(C * 4);
@@ -191,7 +193,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   constexpr int GW = G / FPW, GC = G / 8;     // words, 8-field chunks per group
   extern __shared__ __align__(1024) unsigned char smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int NV = P.NV, NS = P.NS;
+  const int NV = P.NV;
+  constexpr int NS = kNS;
   const int W = P.st.words_per_vec, DP = P.DP, d = P.d, NCH = DP / 8;
   const uint32_t tmem_cols = 2 * NV < 32 ? 32u : (2 * NV <= 64 ? 64u : (2 * NV <= 128 ? 128u : 256u));
   const Layout Lo = make_layout(NV, NS, DP, W, C, KMAX);
@@ -446,23 +449,39 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       if (c.list < 0) break;
       if (c.tile == 0) top.init();
+      // per-column scale ||r|| * 2^-(eT+14) once per tile (NaN marks padding slots)
+      {
+        const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
+        float* nscw = (float*)(sp + Lo.st_nsc);
+        for (int v = et; v < NV; v += kEpiThreads)
+          nscw[v] = v < c.valid ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
+                                : __int_as_float(0x7fc00000);
+        named_bar(1, kEpiThreads);
+      }
       sm100::tc_fence_after();
-      const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
+      const float* nsc = (const float*)(sp + Lo.st_nsc);
       const int* ids = (const int*)(sp + Lo.st_ids);
       const int c0 = half * cols;
 #pragma unroll 1
       for (int cc = 0; cc < cols; cc += kDrain) {
         uint32_t r[kDrain];
         tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
+        float ns[kDrain];
+#pragma unroll
+        for (int e = 0; e < kDrain; e += 4) {
+          const float4 f4 = *(const float4*)(nsc + c0 + cc + e);
+          ns[e] = f4.x;
+          ns[e + 1] = f4.y;
+          ns[e + 2] = f4.z;
+          ns[e + 3] = f4.w;
+        }
         sm100::tmem_ld_wait();
         const float thr = top.s[KMAX - 1];
         int cnt = 0;
 #pragma unroll
         for (int e = 0; e < kDrain; ++e) {
           const int col = c0 + cc + e;
-          const float nsc = col < c.valid ? h2f_bits(nrm[col]) * P.inv_scale
-                                          : __int_as_float(0x7fc00000);
-          const float res = __fmul_rn(__uint_as_float(r[e]), nsc);
+          const float res = __fmul_rn(__uint_as_float(r[e]), ns[e]);
           if (res >= thr) {
             cand_v[cnt * kEpiThreads + et] = res;
             cand_c[cnt * kEpiThreads + et] = col;
@@ -638,7 +657,7 @@ static const size_t kSmemLimit = 227 * 1024;
 static int kmax_for(int depth) { return depth <= 10 ? 10 : 32; }
 
 static bool pick_tile(int DP, int W, int C, int kmax, int* nv, int* ns) {
-  const int cands[6][2] = {{128, 4}, {128, 3}, {64, 4}, {64, 3}, {32, 4}, {32, 3}};
+  const int cands[3][2] = {{128, kNS}, {64, kNS}, {32, kNS}};
   for (auto& c : cands) {
     if (make_layout(c[0], c[1], DP, W, C, kmax).total + 1024 <= kSmemLimit) {
       *nv = c[0];
