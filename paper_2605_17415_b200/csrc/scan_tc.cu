@@ -72,6 +72,7 @@ struct Params {
   int32_t* counter;        // work counter (zeroed per launch)
   double* part_s;          // [nq*n_p*k]
   int32_t* part_id;
+  long long* thr_key;      // [nq] order-preserving key of a lower bound on the k-th score
   int n_p, k, d, DP, NV, NS;
   float t_scale;    // 2^eT
   float inv_scale;  // 2^-(eT+14)
@@ -89,7 +90,7 @@ struct Ctrl {
 
 struct Layout {
   uint32_t qhi, qlo, bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
-      st_qrow, st_nsc, cand, tab, bars, misc, total;
+      st_qrow, st_nsc, cand, tab, thr, bars, misc, total;
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) & ~(a - 1); }
@@ -123,6 +124,7 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.stage = take(L.stage_bytes * NS);
   L.cand = take(cand_entries(KMAX) * kEpiThreads * 8);
   L.tab = take(C * 4);
+  L.thr = take(2 * kM * 4);
   L.bars = take(8 * (2 * 8 + 10));
   L.misc = take(64);
   L.total = off;
@@ -165,6 +167,29 @@ struct RegTopK {
 };
 
 constexpr int gcd_c(int a, int b) { return b ? gcd_c(b, a % b) : a; }
+
+// f64 <-> int64 key preserving order, so atomicMax works on scores
+__device__ __forceinline__ long long dkey(double x) {
+  long long b = __double_as_longlong(x);
+  return b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFLL);
+}
+__device__ __forceinline__ double dkey_inv(long long k) {
+  return __longlong_as_double(k >= 0 ? k : (k ^ 0x7FFFFFFFFFFFFFFFLL));
+}
+
+// Residual-space pruning bound for pair `pi`: a candidate with residual term
+// res < bound has coarse + res < (known lower bound on the query's k-th final
+// score) strictly -- the 1e-12 margin dominates the f64 rounding of
+// coarse + res and nextafterf undoes the f32 conversion's rounding -- so it
+// can never enter the query's top-k, ties included.
+__device__ __forceinline__ float prune_bound(const Params& P, int pi) {
+  if (pi < 0) return -INFINITY;
+  const long long k = *(volatile const long long*)&P.thr_key[pi / P.n_p];
+  const double thr = dkey_inv(k);
+  if (!(thr > -INFINITY)) return -INFINITY;
+  const float b = (float)(thr - P.coarse[pi] - 1e-12);
+  return nextafterf(b, -INFINITY);
+}
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
@@ -437,8 +462,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     const int row = quad * 32 + lane;      // query row == TMEM lane
     float* cand_v = (float*)(smem + Lo.cand);
     int* cand_c = (int*)(smem + Lo.cand + cand_entries(KMAX) * kEpiThreads * 4);
+    float* thr_sh = (float*)(smem + Lo.thr);  // [2][kM] running k-th of each half
     RegTopK<KMAX> top;
     top.init();
+    float bnd = -INFINITY;
     uint32_t t = 0;
     const int cols = NV / 2;
     for (;;) {
@@ -448,7 +475,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       unsigned char* sp = stage(s);
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       if (c.list < 0) break;
-      if (c.tile == 0) top.init();
+      const int pi = ((const int*)(sp + Lo.st_qrow))[row];
+      if (c.tile == 0) {
+        top.init();
+        thr_sh[half * kM + row] = -INFINITY;
+      }
+      if ((c.tile & 3) == 0) bnd = prune_bound(P, pi);
       // per-column scale ||r|| * 2^-(eT+14) once per tile (NaN marks padding slots)
       {
         const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
@@ -476,7 +508,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           ns[e + 3] = f4.w;
         }
         sm100::tmem_ld_wait();
-        const float thr = top.s[KMAX - 1];
+        // a candidate must beat this half's k-th, the other half's k-th (either
+        // bounds the pair's top-k) and the query's global bound from other lists
+        const float thr =
+            fmaxf(fmaxf(top.s[KMAX - 1], *(volatile float*)&thr_sh[(half ^ 1) * kM + row]), bnd);
         int cnt = 0;
 #pragma unroll
         for (int e = 0; e < kDrain; ++e) {
@@ -496,6 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
             if (top.beats(v, id)) top.insert(v, id);
           }
         }
+        if (mx) *(volatile float*)&thr_sh[half * kM + row] = top.s[KMAX - 1];
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -517,17 +553,22 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
             const int id = cand_c[p * kEpiThreads + et + 128];
             if (id != INT_MAX && top.beats(v, id)) top.insert(v, id);
           }
-          const int pi = ((const int*)(sp + Lo.st_qrow))[row];
           const double cs = P.coarse[pi];
           const int64_t o = (int64_t)pi * P.k;
+          float kth = -INFINITY;
 #pragma unroll
           for (int p = 0; p < KMAX; ++p) {
             if (p < P.k) {
               const bool have = top.i[p] != INT_MAX;
               P.part_s[o + p] = have ? cs + (double)top.s[p] : -INFINITY;
               P.part_id[o + p] = have ? top.i[p] : INT_MAX;
+              if (p == P.k - 1 && have) kth = top.s[p];
             }
           }
+          // this pair alone holds k candidates >= kth: a global lower bound on
+          // the query's final k-th score, pruning its other lists
+          if (kth > -INFINITY)
+            atomicMax(&P.thr_key[pi / P.n_p], dkey(cs + (double)kth));
         }
         named_bar(1, kEpiThreads);
       }
@@ -541,24 +582,37 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
 }
 
 // ---- probe regrouping: pairs (q, p) bucketed by list ---------------------------
-__global__ void pair_count_kernel(const int32_t* __restrict__ probe, int64_t npairs,
-                                  int32_t* __restrict__ cnt) {
+// Pairs are ordered inside each list by probe-rank class (rank 0..6, then 7+)
+// and work items are emitted tile-major (every list's first query tile before
+// any second tile). A query's best-ranked lists are therefore scanned first,
+// which tightens its global pruning bound (thr_key) before its far lists run.
+constexpr int kRC = 8;
+
+__global__ void pair_count_kernel(const int32_t* __restrict__ probe, int64_t npairs, int n_p,
+                                  int32_t* __restrict__ cnt2) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < npairs) atomicAdd(&cnt[probe[i]], 1);
+  if (i >= npairs) return;
+  const int rc = min((int)(i % n_p), kRC - 1);
+  atomicAdd(&cnt2[probe[i] * kRC + rc], 1);
 }
 
-// one block: exclusive scans of counts and of query tiles per list
-__global__ void __launch_bounds__(1024) pair_scan_kernel(const int32_t* __restrict__ cnt, int L,
+// one block: exclusive scan over (list, rank class); per-list starts, tiles,
+// and the per-tile-index list counts G[t]
+__global__ void __launch_bounds__(1024) pair_scan_kernel(const int32_t* __restrict__ cnt2, int L,
+                                                         int32_t* __restrict__ pstart2,
                                                          int32_t* __restrict__ pstart,
-                                                         int32_t* __restrict__ istart,
+                                                         int32_t* __restrict__ ntile,
+                                                         int32_t* __restrict__ G,
                                                          int32_t* __restrict__ n_items) {
   __shared__ int sa[1024], sb[1024];
   const int per = (L + 1023) / 1024;
-  const int b0 = threadIdx.x * per;
+  const int l0 = threadIdx.x * per, l1 = min(L, l0 + per);
   int a = 0, t = 0;
-  for (int i = b0; i < min(L, b0 + per); ++i) {
-    a += cnt[i];
-    t += (cnt[i] + kM - 1) / kM;
+  for (int l = l0; l < l1; ++l) {
+    int c = 0;
+    for (int r = 0; r < kRC; ++r) c += cnt2[l * kRC + r];
+    a += c;
+    t += (c + kM - 1) / kM;
   }
   sa[threadIdx.x] = a;
   sb[threadIdx.x] = t;
@@ -572,36 +626,68 @@ __global__ void __launch_bounds__(1024) pair_scan_kernel(const int32_t* __restri
     __syncthreads();
   }
   a = sa[threadIdx.x] - a;  // exclusive
-  t = sb[threadIdx.x] - t;
-  for (int i = b0; i < min(L, b0 + per); ++i) {
-    pstart[i] = a;
-    istart[i] = t;
-    a += cnt[i];
-    t += (cnt[i] + kM - 1) / kM;
+  for (int l = l0; l < l1; ++l) {
+    pstart[l] = a;
+    int c = 0;
+    for (int r = 0; r < kRC; ++r) {
+      pstart2[l * kRC + r] = a + c;
+      c += cnt2[l * kRC + r];
+    }
+    const int nt = (c + kM - 1) / kM;
+    ntile[l] = nt;
+    for (int i = 0; i < nt; ++i) atomicAdd(&G[i], 1);
+    a += c;
   }
   if (threadIdx.x == 1023) {
     pstart[L] = sa[1023];
-    istart[L] = sb[1023];
+    pstart2[L * kRC] = sa[1023];
     *n_items = sb[1023];
   }
 }
 
-__global__ void pair_scatter_kernel(const int32_t* __restrict__ probe, int64_t npairs,
-                                    const int32_t* __restrict__ pstart,
-                                    int32_t* __restrict__ cursor, int32_t* __restrict__ pairs) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= npairs) return;
-  int l = probe[i];
-  pairs[pstart[l] + atomicAdd(&cursor[l], 1)] = (int32_t)i;
+// one block: exclusive scan of G -> S (first item slot of each tile index)
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const int32_t* __restrict__ G, int T,
+                                                         int32_t* __restrict__ S) {
+  __shared__ int sa[1024];
+  const int per = (T + 1023) / 1024;
+  const int t0 = threadIdx.x * per, t1 = min(T, t0 + per);
+  int a = 0;
+  for (int t = t0; t < t1; ++t) a += G[t];
+  sa[threadIdx.x] = a;
+  __syncthreads();
+  for (int s = 1; s < 1024; s <<= 1) {
+    int v = threadIdx.x >= s ? sa[threadIdx.x - s] : 0;
+    __syncthreads();
+    sa[threadIdx.x] += v;
+    __syncthreads();
+  }
+  a = sa[threadIdx.x] - a;
+  for (int t = t0; t < t1; ++t) {
+    S[t] = a;
+    a += G[t];
+  }
 }
 
-__global__ void items_fill_kernel(const int32_t* __restrict__ cnt,
-                                  const int32_t* __restrict__ istart, int L,
-                                  int2* __restrict__ items) {
+__global__ void pair_scatter_kernel(const int32_t* __restrict__ probe, int64_t npairs, int n_p,
+                                    const int32_t* __restrict__ pstart2,
+                                    int32_t* __restrict__ cursor2, int32_t* __restrict__ pairs) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= npairs) return;
+  const int b = probe[i] * kRC + min((int)(i % n_p), kRC - 1);
+  pairs[pstart2[b] + atomicAdd(&cursor2[b], 1)] = (int32_t)i;
+}
+
+__global__ void items_fill_kernel(const int32_t* __restrict__ ntile, const int32_t* __restrict__ S,
+                                  int32_t* __restrict__ fill, int L, int2* __restrict__ items) {
   int l = blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= L) return;
-  int t = (cnt[l] + kM - 1) / kM, b = istart[l];
-  for (int i = 0; i < t; ++i) items[b + i] = make_int2(l, i);
+  const int nt = ntile[l];
+  for (int t = 0; t < nt; ++t) items[S[t] + atomicAdd(&fill[t], 1)] = make_int2(l, t);
+}
+
+__global__ void thr_init_kernel(long long* __restrict__ key, int64_t n) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) key[i] = dkey(-INFINITY);
 }
 
 }  // namespace tc
@@ -615,10 +701,13 @@ static int g_num_sms = 0;
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct TcScratch {
-  int32_t *cnt, *cursor, *pstart, *istart, *n_items, *counter, *pairs;
+  int32_t *cnt2, *cursor2, *G, *fill, *counter, *pstart2, *pstart, *ntile, *S, *n_items, *pairs;
+  long long* thr_key;
   int2* items;
   double* part_s;
   int32_t* part_id;
+  char* zero_end;
+  int T;
   size_t bytes;
 };
 
@@ -628,17 +717,25 @@ static TcScratch carve_tc(void* base, int64_t nq, int n_p, int L, int k) {
   char* b = (char*)base;
   int64_t np = nq * n_p;
   int64_t max_items = np / kM + (np < L ? np : L) + 1;
+  S.T = (int)(nq / kM + 2);
   auto take = [&](size_t bytes) {
     char* p = b ? b + off : nullptr;
     off += align256(bytes);
     return p;
   };
-  S.cnt = (int32_t*)take(4 * (size_t)L);
-  S.cursor = (int32_t*)take(4 * (size_t)L);
+  // zero-initialised block first
+  S.cnt2 = (int32_t*)take(4 * (size_t)L * kRC);
+  S.cursor2 = (int32_t*)take(4 * (size_t)L * kRC);
+  S.G = (int32_t*)take(4 * (size_t)S.T);
+  S.fill = (int32_t*)take(4 * (size_t)S.T);
   S.counter = (int32_t*)take(16);
+  S.zero_end = b ? b + off : nullptr;
+  S.pstart2 = (int32_t*)take(4 * ((size_t)L * kRC + 1));
   S.pstart = (int32_t*)take(4 * (size_t)(L + 1));
-  S.istart = (int32_t*)take(4 * (size_t)(L + 1));
+  S.ntile = (int32_t*)take(4 * (size_t)L);
+  S.S = (int32_t*)take(4 * (size_t)(S.T + 1));
   S.n_items = (int32_t*)take(16);
+  S.thr_key = (long long*)take(8 * (size_t)nq);
   S.pairs = (int32_t*)take(4 * (size_t)np);
   S.items = (int2*)take(8 * (size_t)max_items);
   S.part_s = (double*)take(8 * (size_t)np * k);
@@ -713,15 +810,19 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   }
   TcScratch S = carve_tc(scratch, nq, n_p, L, depth);
   int64_t np = nq * n_p;
-  IVFTQ_CHECK_CUDA(cudaMemsetAsync(S.cnt, 0, (char*)S.pstart - (char*)S.cnt, s));
+  IVFTQ_CHECK_CUDA(cudaMemsetAsync(S.cnt2, 0, S.zero_end - (char*)S.cnt2, s));
   unsigned gp = (unsigned)((np + 255) / 256);
-  pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, S.cnt);
+  thr_init_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(S.thr_key, nq);
+  if (int e = check_launch("thr_init")) return e;
+  pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.cnt2);
   if (int e = check_launch("pair_count")) return e;
-  pair_scan_kernel<<<1, 1024, 0, s>>>(S.cnt, L, S.pstart, S.istart, S.n_items);
+  pair_scan_kernel<<<1, 1024, 0, s>>>(S.cnt2, L, S.pstart2, S.pstart, S.ntile, S.G, S.n_items);
   if (int e = check_launch("pair_scan")) return e;
-  pair_scatter_kernel<<<gp, 256, 0, s>>>(probe, np, S.pstart, S.cursor, S.pairs);
+  tile_scan_kernel<<<1, 1024, 0, s>>>(S.G, S.T, S.S);
+  if (int e = check_launch("tile_scan")) return e;
+  pair_scatter_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.pstart2, S.cursor2, S.pairs);
   if (int e = check_launch("pair_scatter")) return e;
-  items_fill_kernel<<<(L + 255) / 256, 256, 0, s>>>(S.cnt, S.istart, L, S.items);
+  items_fill_kernel<<<(L + 255) / 256, 256, 0, s>>>(S.ntile, S.S, S.fill, L, S.items);
   if (int e = check_launch("items_fill")) return e;
 
   const int fb = st->field_bits, C = 1 << fb;
@@ -740,6 +841,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   P.counter = S.counter;
   P.part_s = S.part_s;
   P.part_id = S.part_id;
+  P.thr_key = S.thr_key;
   P.n_p = n_p;
   P.k = depth;
   P.d = st->dim;
