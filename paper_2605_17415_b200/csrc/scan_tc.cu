@@ -51,11 +51,11 @@ namespace tc {
 constexpr int kM = 128;          // queries per item = MMA M
 constexpr int kProdWarp = 0;     // producer (TMA + control records)
 constexpr int kMmaWarp = 1;      // tcgen05.mma issuer, owns TMEM
-constexpr int kDecWarp0 = 2;     // decoder warps 2..5
-constexpr int kDecWarps = 4;
-constexpr int kEpiWarp0 = 6;     // epilogue warps 6..13
+constexpr int kDecWarp0 = 2;     // decoder warps 2..9
+constexpr int kDecWarps = 8;
+constexpr int kEpiWarp0 = 10;    // epilogue warps 10..17
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 448
+constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 576
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
 constexpr int kNS = 4;           // stage ring depth (power of two)
@@ -90,7 +90,7 @@ struct Ctrl {
 
 struct Layout {
   uint32_t qhi, qlo, bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
-      st_qrow, st_nsc, cand, tab, thr, bars, misc, total;
+      st_qrow, meta[2], meta_bytes, m_nsc, m_ids, m_qrow, cand, tab, thr, bars, misc, total;
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) & ~(a - 1); }
@@ -119,13 +119,19 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.st_ids = L.st_norms + align_up(NV * 2, 128);
   L.st_ctrl = L.st_ids + align_up(NV * 4, 128);
   L.st_qrow = L.st_ctrl + 128;
-  L.st_nsc = L.st_qrow + kM * 4;
-  L.stage_bytes = L.st_nsc + align_up(NV * 4, 128);
+  L.stage_bytes = L.st_qrow + kM * 4;
   L.stage = take(L.stage_bytes * NS);
+  // per-accumulator-buffer epilogue record: ctrl | nsc | ids | qrow
+  L.m_nsc = 128;
+  L.m_ids = L.m_nsc + align_up(NV * 4, 128);
+  L.m_qrow = L.m_ids + align_up(NV * 4, 128);
+  L.meta_bytes = L.m_qrow + kM * 4;
+  L.meta[0] = take(L.meta_bytes);
+  L.meta[1] = take(L.meta_bytes);
   L.cand = take(cand_entries(KMAX) * kEpiThreads * 8);
   L.tab = take(C * 4);
   L.thr = take(2 * kM * 4);
-  L.bars = take(8 * (2 * 8 + 10));
+  L.bars = take(8 * 32);
   L.misc = take(64);
   L.total = off;
   return L;
@@ -233,7 +239,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   uint64_t* acc_empty = bars + 22;     // [2] epilogue -> MMA
   uint64_t* a_full = bars + 24;        // decoders -> MMA (A operand built)
   uint64_t* a_empty = bars + 25;       // MMA commit -> decoders (A operand free)
+  uint64_t* meta_full = bars + 26;     // [2] decoders -> epilogue (tile record)
+  uint64_t* meta_empty = bars + 28;    // [2] epilogue -> decoders
   uint32_t* tmem_slot = (uint32_t*)(smem + Lo.misc);
+  for (int i = tid; i < 2 * kM; i += kThreads) ((float*)(smem + Lo.thr))[i] = -INFINITY;
+  auto meta = [&](int b) { return smem + (b ? Lo.meta[1] : Lo.meta[0]); };
   auto stage = [&](int s) { return smem + Lo.stage + (uint32_t)s * Lo.stage_bytes; };
 
   // ---- one-time setup ---------------------------------------------------------
@@ -246,13 +256,15 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       sm100::mbar_init(&st_full[s], 1);
-      sm100::mbar_init(&st_empty[s], kDecWarps + kEpiWarps);
+      sm100::mbar_init(&st_empty[s], kDecWarps);
     }
     for (int b = 0; b < 2; ++b) {
       sm100::mbar_init(&op_full[b], kDecWarps);
       sm100::mbar_init(&op_empty[b], 1);
       sm100::mbar_init(&acc_full[b], 1);
       sm100::mbar_init(&acc_empty[b], kEpiWarps);
+      sm100::mbar_init(&meta_full[b], kDecWarps);
+      sm100::mbar_init(&meta_empty[b], kEpiWarps);
     }
     sm100::mbar_init(a_full, kDecWarps);
     sm100::mbar_init(a_empty, 1);
@@ -333,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     for (;;) {
       const int ob = t & 1;
       sm100::mbar_wait(&op_full[ob], (t >> 1) & 1);
-      const Ctrl c = *(const Ctrl*)(stage(t % NS) + Lo.st_ctrl);
+      const Ctrl c = *(const Ctrl*)(meta(ob));
       if (t >= 2) sm100::mbar_wait(&acc_empty[ob], ((t >> 1) - 1) & 1);
       if (c.list < 0) {
         if (lane == 0) mbar_arrive(&acc_full[ob]);
@@ -380,6 +392,30 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       const int ob = t & 1;
       if (t >= 2) sm100::mbar_wait(&op_empty[ob], ((t >> 1) - 1) & 1);
+      // ---- tile record for the MMA issuer and the epilogue (frees the stage
+      //      slot for the producer as soon as decoding is done) --------------------
+      if (t >= 2) sm100::mbar_wait(&meta_empty[ob], ((t >> 1) - 1) & 1);
+      {
+        unsigned char* mp = meta(ob);
+        if (dt_ == 0) *(Ctrl*)mp = c;
+        if (c.list >= 0) {
+          const int* qsrc = (const int*)(sp + Lo.st_qrow);
+          const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
+          const int* idsrc = (const int*)(sp + Lo.st_ids);
+          int* qdst = (int*)(mp + Lo.m_qrow);
+          float* nsc = (float*)(mp + Lo.m_nsc);
+          int* idd = (int*)(mp + Lo.m_ids);
+          for (int i = dt_; i < kM; i += kDecThreads) qdst[i] = qsrc[i];
+          for (int v = dt_; v < NV; v += kDecThreads) {
+            const bool ok = v < c.valid;
+            nsc[v] = ok ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
+                        : __int_as_float(0x7fc00000);
+            idd[v] = ok ? idsrc[v] : INT_MAX;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&meta_full[ob]);
+      }
       if (c.list < 0) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&op_full[ob]);
@@ -469,30 +505,18 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0;
     const int cols = NV / 2;
     for (;;) {
-      const int ab = t & 1, s = t % NS;
+      const int ab = t & 1;
       sm100::mbar_wait(&acc_full[ab], (t >> 1) & 1);
-      sm100::mbar_wait(&st_full[s], (t / NS) & 1);
-      unsigned char* sp = stage(s);
-      const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
+      sm100::mbar_wait(&meta_full[ab], (t >> 1) & 1);
+      const unsigned char* mp = meta(ab);
+      const Ctrl c = *(const Ctrl*)mp;
       if (c.list < 0) break;
-      const int pi = ((const int*)(sp + Lo.st_qrow))[row];
-      if (c.tile == 0) {
-        top.init();
-        thr_sh[half * kM + row] = -INFINITY;
-      }
+      const int pi = ((const int*)(mp + Lo.m_qrow))[row];
+      if (c.tile == 0) top.init();
       if ((c.tile & 3) == 0) bnd = prune_bound(P, pi);
-      // per-column scale ||r|| * 2^-(eT+14) once per tile (NaN marks padding slots)
-      {
-        const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
-        float* nscw = (float*)(sp + Lo.st_nsc);
-        for (int v = et; v < NV; v += kEpiThreads)
-          nscw[v] = v < c.valid ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
-                                : __int_as_float(0x7fc00000);
-        named_bar(1, kEpiThreads);
-      }
       sm100::tc_fence_after();
-      const float* nsc = (const float*)(sp + Lo.st_nsc);
-      const int* ids = (const int*)(sp + Lo.st_ids);
+      const float* nsc = (const float*)(mp + Lo.m_nsc);
+      const int* ids = (const int*)(mp + Lo.m_ids);
       const int c0 = half * cols;
 #pragma unroll 1
       for (int cc = 0; cc < cols; cc += kDrain) {
@@ -555,25 +579,27 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           }
           const double cs = P.coarse[pi];
           const int64_t o = (int64_t)pi * P.k;
-          float kth = -INFINITY;
 #pragma unroll
           for (int p = 0; p < KMAX; ++p) {
             if (p < P.k) {
               const bool have = top.i[p] != INT_MAX;
               P.part_s[o + p] = have ? cs + (double)top.s[p] : -INFINITY;
               P.part_id[o + p] = have ? top.i[p] : INT_MAX;
-              if (p == P.k - 1 && have) kth = top.s[p];
             }
           }
-          // this pair alone holds k candidates >= kth: a global lower bound on
-          // the query's final k-th score, pruning its other lists
-          if (kth > -INFINITY)
-            atomicMax(&P.thr_key[pi / P.n_p], dkey(cs + (double)kth));
+          // this pair alone holds KMAX >= k candidates >= its KMAX-th score:
+          // a global lower bound on the query's final k-th, pruning its other
+          // lists (static index keeps the top-K in registers)
+          if (top.i[KMAX - 1] != INT_MAX)
+            atomicMax(&P.thr_key[pi / P.n_p], dkey(cs + (double)top.s[KMAX - 1]));
         }
+        // reset the shared half thresholds for the next item before anyone
+        // can read them again (next read follows this barrier)
+        thr_sh[half * kM + row] = -INFINITY;
         named_bar(1, kEpiThreads);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&st_empty[s]);
+      if (lane == 0) mbar_arrive(&meta_empty[ab]);
       ++t;
     }
   }
