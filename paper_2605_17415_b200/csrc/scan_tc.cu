@@ -59,6 +59,7 @@ constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 576
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
 constexpr int kNS = 4;           // stage ring depth (power of two)
+constexpr int kMeta = 4;         // tile-record ring depth (power of two)
 
 struct Params {
   ivftq_store st;
@@ -90,7 +91,7 @@ struct Ctrl {
 
 struct Layout {
   uint32_t qhi, qlo, bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
-      st_qrow, meta[2], meta_bytes, m_nsc, m_ids, m_qrow, cand, tab, thr, bars, misc, total;
+      st_qrow, meta0, meta_bytes, m_nsc, m_ids, m_qrow, cand, tab, thr, bars, misc, total;
 };
 
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) & ~(a - 1); }
@@ -125,13 +126,12 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.m_nsc = 128;
   L.m_ids = L.m_nsc + align_up(NV * 4, 128);
   L.m_qrow = L.m_ids + align_up(NV * 4, 128);
-  L.meta_bytes = L.m_qrow + kM * 4;
-  L.meta[0] = take(L.meta_bytes);
-  L.meta[1] = take(L.meta_bytes);
+  L.meta_bytes = align_up(L.m_qrow + kM * 4, 128);
+  L.meta0 = take(L.meta_bytes * kMeta);
   L.cand = take(cand_entries(KMAX) * kEpiThreads * 8);
   L.tab = take(C * 4);
   L.thr = take(2 * kM * 4);
-  L.bars = take(8 * 32);
+  L.bars = take(8 * 40);
   L.misc = take(64);
   L.total = off;
   return L;
@@ -239,11 +239,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   uint64_t* acc_empty = bars + 22;     // [2] epilogue -> MMA
   uint64_t* a_full = bars + 24;        // decoders -> MMA (A operand built)
   uint64_t* a_empty = bars + 25;       // MMA commit -> decoders (A operand free)
-  uint64_t* meta_full = bars + 26;     // [2] decoders -> epilogue (tile record)
-  uint64_t* meta_empty = bars + 28;    // [2] epilogue -> decoders
+  uint64_t* meta_full = bars + 26;     // [kMeta] decoders -> MMA/epilogue (tile record)
+  uint64_t* meta_empty = bars + 30;    // [kMeta] epilogue -> decoders
   uint32_t* tmem_slot = (uint32_t*)(smem + Lo.misc);
   for (int i = tid; i < 2 * kM; i += kThreads) ((float*)(smem + Lo.thr))[i] = -INFINITY;
-  auto meta = [&](int b) { return smem + (b ? Lo.meta[1] : Lo.meta[0]); };
+  auto meta = [&](int m) { return smem + Lo.meta0 + (uint32_t)m * Lo.meta_bytes; };
   auto stage = [&](int s) { return smem + Lo.stage + (uint32_t)s * Lo.stage_bytes; };
 
   // ---- one-time setup ---------------------------------------------------------
@@ -263,8 +263,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       sm100::mbar_init(&op_empty[b], 1);
       sm100::mbar_init(&acc_full[b], 1);
       sm100::mbar_init(&acc_empty[b], kEpiWarps);
-      sm100::mbar_init(&meta_full[b], kDecWarps);
-      sm100::mbar_init(&meta_empty[b], kEpiWarps);
+    }
+    for (int m = 0; m < kMeta; ++m) {
+      sm100::mbar_init(&meta_full[m], kDecWarps);
+      sm100::mbar_init(&meta_empty[m], kEpiWarps);
     }
     sm100::mbar_init(a_full, kDecWarps);
     sm100::mbar_init(a_empty, 1);
@@ -345,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     for (;;) {
       const int ob = t & 1;
       sm100::mbar_wait(&op_full[ob], (t >> 1) & 1);
-      const Ctrl c = *(const Ctrl*)(meta(ob));
+      const Ctrl c = *(const Ctrl*)(meta(t & (kMeta - 1)));
       if (t >= 2) sm100::mbar_wait(&acc_empty[ob], ((t >> 1) - 1) & 1);
       if (c.list < 0) {
         if (lane == 0) mbar_arrive(&acc_full[ob]);
@@ -392,11 +394,13 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       const int ob = t & 1;
       if (t >= 2) sm100::mbar_wait(&op_empty[ob], ((t >> 1) - 1) & 1);
-      // ---- tile record for the MMA issuer and the epilogue (frees the stage
-      //      slot for the producer as soon as decoding is done) --------------------
-      if (t >= 2) sm100::mbar_wait(&meta_empty[ob], ((t >> 1) - 1) & 1);
+      if (c.list < 0) {
+        // ---- tile record for the MMA issuer and the epilogue (copied out so the
+      //      stage slot returns to the producer as soon as decoding is done) ------
+      const int ms = t & (kMeta - 1);
+      if (t >= (uint32_t)kMeta) sm100::mbar_wait(&meta_empty[ms], ((t / kMeta) - 1) & 1);
       {
-        unsigned char* mp = meta(ob);
+        unsigned char* mp = meta(ms);
         if (dt_ == 0) *(Ctrl*)mp = c;
         if (c.list >= 0) {
           const int* qsrc = (const int*)(sp + Lo.st_qrow);
@@ -414,9 +418,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&meta_full[ob]);
+        if (lane == 0) mbar_arrive(&meta_full[ms]);
       }
-      if (c.list < 0) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&op_full[ob]);
         break;
@@ -483,6 +486,31 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         }
       }
       sm100::fence_proxy_async_smem();
+      // ---- tile record for the MMA issuer and the epilogue (copied out so the
+      //      stage slot returns to the producer as soon as decoding is done) ------
+      const int ms = t & (kMeta - 1);
+      if (t >= (uint32_t)kMeta) sm100::mbar_wait(&meta_empty[ms], ((t / kMeta) - 1) & 1);
+      {
+        unsigned char* mp = meta(ms);
+        if (dt_ == 0) *(Ctrl*)mp = c;
+        if (c.list >= 0) {
+          const int* qsrc = (const int*)(sp + Lo.st_qrow);
+          const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
+          const int* idsrc = (const int*)(sp + Lo.st_ids);
+          int* qdst = (int*)(mp + Lo.m_qrow);
+          float* nsc = (float*)(mp + Lo.m_nsc);
+          int* idd = (int*)(mp + Lo.m_ids);
+          for (int i = dt_; i < kM; i += kDecThreads) qdst[i] = qsrc[i];
+          for (int v = dt_; v < NV; v += kDecThreads) {
+            const bool ok = v < c.valid;
+            nsc[v] = ok ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
+                        : __int_as_float(0x7fc00000);
+            idd[v] = ok ? idsrc[v] : INT_MAX;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&meta_full[ms]);
+      }
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(&op_full[ob]);
@@ -505,10 +533,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0;
     const int cols = NV / 2;
     for (;;) {
-      const int ab = t & 1;
+      const int ab = t & 1, ms = t & (kMeta - 1);
       sm100::mbar_wait(&acc_full[ab], (t >> 1) & 1);
-      sm100::mbar_wait(&meta_full[ab], (t >> 1) & 1);
-      const unsigned char* mp = meta(ab);
+      sm100::mbar_wait(&meta_full[ms], (t / kMeta) & 1);
+      const unsigned char* mp = meta(ms);
       const Ctrl c = *(const Ctrl*)mp;
       if (c.list < 0) break;
       const int pi = ((const int*)(mp + Lo.m_qrow))[row];
@@ -599,7 +627,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         named_bar(1, kEpiThreads);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&meta_empty[ab]);
+      if (lane == 0) mbar_arrive(&meta_empty[ms]);
       ++t;
     }
   }
