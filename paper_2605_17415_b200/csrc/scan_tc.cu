@@ -34,6 +34,7 @@
 // same order as the reference's own f32 sgemm. The residual term is then
 // D * (2^-(eT+14) * f32(||r||)), the candidate score coarse + (double)res.
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 
 #include "common.cuh"
@@ -60,6 +61,10 @@ constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
 constexpr int kNS = 4;           // stage ring depth (power of two)
 constexpr int kMeta = 4;         // tile-record ring depth (power of two)
+constexpr int kAcc = 4;          // TMEM accumulator ring depth (power of two)
+constexpr int kNV = 64;          // vectors per tile (MMA N)
+// TMEM budget: kAcc accumulators of kNV columns + the A operand (DP columns)
+constexpr int kMaxDim = 512 - kAcc * kNV;
 
 struct Params {
   ivftq_store st;
@@ -74,6 +79,9 @@ struct Params {
   double* part_s;          // [nq*n_p*k]
   int32_t* part_id;
   long long* thr_key;      // [nq] order-preserving key of a lower bound on the k-th score
+  long long* trace;        // debug timeline of CTA 0 (IVFTQ_TRACE), else null
+  const uint32_t* q_hi;    // [nq][DP/2] rotated query rows, fp16 hi halves (x 2^14), packed pairs
+  const uint32_t* q_lo;    // [nq][DP/2] matching lo halves
   int n_p, k, d, DP, NV, NS;
   float t_scale;    // 2^eT
   float inv_scale;  // 2^-(eT+14)
@@ -90,7 +98,7 @@ struct Ctrl {
 };
 
 struct Layout {
-  uint32_t qhi, qlo, bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
+  uint32_t bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
       st_qrow, meta0, meta_bytes, m_nsc, m_ids, m_qrow, cand, tab, thr, bars, misc, total;
 };
 
@@ -108,8 +116,6 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
     off = align_up(off + bytes, 128u);
     return o;
   };
-  L.qhi = take(kM * DP * 2);
-  L.qlo = take(kM * DP * 2);
   for (int b = 0; b < 2; ++b) {
     L.bhi[b] = take(NV * DP * 2);
     L.blo[b] = take(NV * DP * 2);
@@ -131,7 +137,7 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.cand = take(cand_entries(KMAX) * kEpiThreads * 8);
   L.tab = take(C * 4);
   L.thr = take(2 * kM * 4);
-  L.bars = take(8 * 40);
+  L.bars = take(8 * 48);
   L.misc = take(64);
   L.total = off;
   return L;
@@ -173,6 +179,13 @@ struct RegTopK {
 };
 
 constexpr int gcd_c(int a, int b) { return b ? gcd_c(b, a % b) : a; }
+
+constexpr int kTraceTiles = 4096;
+#define TRACE(slot)                                                              \
+  do {                                                                           \
+    if (P.trace && blockIdx.x == 0 && lane == 0 && t < (uint32_t)kTraceTiles)    \
+      P.trace[t * 8 + (slot)] = clock64();                                       \
+  } while (0)
 
 // f64 <-> int64 key preserving order, so atomicMax works on scores
 __device__ __forceinline__ long long dkey(double x) {
@@ -227,7 +240,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   const int NV = P.NV;
   constexpr int NS = kNS;
   const int W = P.st.words_per_vec, DP = P.DP, d = P.d, NCH = DP / 8;
-  const uint32_t tmem_cols = 2 * NV < 32 ? 32u : (2 * NV <= 64 ? 64u : (2 * NV <= 128 ? 128u : 256u));
+  // TMEM columns: kAcc accumulators of NV columns, then the A operand
+  // (Qhi, Qlo: DP/2 columns each)
+  const uint32_t a_col = kAcc * NV;
+  const uint32_t need = a_col + DP;
+  const uint32_t tmem_cols = need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
   const Layout Lo = make_layout(NV, NS, DP, W, C, KMAX);
   uint32_t* tab = (uint32_t*)(smem + Lo.tab);
   uint64_t* bars = (uint64_t*)(smem + Lo.bars);
@@ -235,8 +252,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   uint64_t* st_empty = bars + 8;       // [NS] decoders + epilogue -> producer
   uint64_t* op_full = bars + 16;       // [2] decoders -> MMA
   uint64_t* op_empty = bars + 18;      // [2] MMA commit -> decoders
-  uint64_t* acc_full = bars + 20;      // [2] MMA commit -> epilogue
-  uint64_t* acc_empty = bars + 22;     // [2] epilogue -> MMA
+  uint64_t* acc_full = bars + 36;      // [kAcc] MMA commit -> epilogue
+  uint64_t* acc_empty = bars + 40;     // [kAcc] epilogue -> MMA
   uint64_t* a_full = bars + 24;        // decoders -> MMA (A operand built)
   uint64_t* a_empty = bars + 25;       // MMA commit -> decoders (A operand free)
   uint64_t* meta_full = bars + 26;     // [kMeta] decoders -> MMA/epilogue (tile record)
@@ -261,6 +278,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     for (int b = 0; b < 2; ++b) {
       sm100::mbar_init(&op_full[b], kDecWarps);
       sm100::mbar_init(&op_empty[b], 1);
+    }
+    for (int b = 0; b < kAcc; ++b) {
       sm100::mbar_init(&acc_full[b], 1);
       sm100::mbar_init(&acc_empty[b], kEpiWarps);
     }
@@ -335,22 +354,24 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           sm100::bulk_g2s(sp + Lo.st_codes, P.st.codes + (s0 >> 5) * W * 32, cb, &st_full[s]);
           sm100::bulk_g2s(sp + Lo.st_norms, P.st.norms + s0, nb, &st_full[s]);
           sm100::bulk_g2s(sp + Lo.st_ids, P.st.ids + s0, ib, &st_full[s]);
+          TRACE(0);
         }
       }
     }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer ===============================================
     const uint32_t idesc = sm100::idesc_f16_f32(kM, NV);
-    const uint32_t a_lbo = kM * 16, b_lbo = NV * 16, sbo = 128;
-    const uint32_t qhi_a = sm100::smem_u32(smem + Lo.qhi), qlo_a = sm100::smem_u32(smem + Lo.qlo);
+    const uint32_t b_lbo = NV * 16, sbo = 128;
+    const uint32_t qhi_t = tmem + a_col, qlo_t = tmem + a_col + DP / 2;  // A in TMEM
     uint32_t t = 0, u = 0;
     for (;;) {
       const int ob = t & 1;
       sm100::mbar_wait(&op_full[ob], (t >> 1) & 1);
       const Ctrl c = *(const Ctrl*)(meta(t & (kMeta - 1)));
-      if (t >= 2) sm100::mbar_wait(&acc_empty[ob], ((t >> 1) - 1) & 1);
+      const int ab = t & (kAcc - 1);
+      if (t >= (uint32_t)kAcc) sm100::mbar_wait(&acc_empty[ab], ((t / kAcc) - 1) & 1);
       if (c.list < 0) {
-        if (lane == 0) mbar_arrive(&acc_full[ob]);
+        if (lane == 0) mbar_arrive(&acc_full[ab]);
         break;
       }
       if (c.tile == 0) {
@@ -358,25 +379,27 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         ++u;
       }
       sm100::tc_fence_after();
+      TRACE(3);
       if (lane == 0) {
         const uint32_t bh = sm100::smem_u32(smem + (ob ? Lo.bhi[1] : Lo.bhi[0]));
         const uint32_t bl = sm100::smem_u32(smem + (ob ? Lo.blo[1] : Lo.blo[0]));
-        const uint32_t dt = tmem + ob * NV;
+        const uint32_t dt = tmem + ab * NV;
         const int ks = DP / 16;
         uint32_t acc = 0;
         for (int pass = 0; pass < 3; ++pass) {
-          const uint32_t aa = pass == 1 ? qlo_a : qhi_a;
+          const uint32_t at = pass == 1 ? qlo_t : qhi_t;
           const uint32_t ba = pass == 2 ? bl : bh;
           for (int s = 0; s < ks; ++s) {
-            uint64_t ad = sm100::smem_desc(aa + s * 2 * a_lbo, a_lbo, sbo);
+            // K step s: 16 fp16 = 8 TMEM columns of A, two 16-byte chunks of B
             uint64_t bd = sm100::smem_desc(ba + s * 2 * b_lbo, b_lbo, sbo);
-            sm100::mma_f16(dt, ad, bd, idesc, acc);
+            sm100::mma_f16_ts(dt, at + s * 8, bd, idesc, acc);
             acc = 1;
           }
         }
         sm100::mma_commit(&op_empty[ob]);
-        sm100::mma_commit(&acc_full[ob]);
+        sm100::mma_commit(&acc_full[ab]);
         if (c.tile == c.ntiles - 1) sm100::mma_commit(a_empty);
+        TRACE(4);
       }
       __syncwarp();
       ++t;
@@ -390,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     for (;;) {
       const int s = t % NS;
       sm100::mbar_wait(&st_full[s], (t / NS) & 1);
+      if (warp == kDecWarp0) TRACE(1);
       unsigned char* sp = stage(s);
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       const int ob = t & 1;
@@ -426,27 +450,34 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       }
       if (c.tile == 0) {
         // A operand for the new item: wait until the previous item's MMAs are done
+        // A lives in TMEM: lane = query row, 2 fp16 per 32-bit column along K.
+        // Decoder warp w writes TMEM lane quadrant w%4; warps 2..5 the hi
+        // halves, 6..9 the lo halves, straight from the pre-split rows.
         if (u > 0) sm100::mbar_wait(a_empty, (u - 1) & 1);
-        const int* qrow = (const int*)(sp + Lo.st_qrow);
-        for (int task = dt_; task < kM * NCH; task += kDecThreads) {
-          const int r = task % kM, ch = task / kM;
-          const int pi = qrow[r];
-          uint32_t h[8], lw[8];
-          const float* qv = pi >= 0 ? P.qrot + (int64_t)(pi / P.n_p) * d : nullptr;
+        sm100::tc_fence_after();
+        {
+          const int part = (warp - kDecWarp0) >> 2;  // 0 = hi, 1 = lo
+          const int rrow = (warp & 3) * 32 + lane;
+          const int pi = ((const int*)(sp + Lo.st_qrow))[rrow];
+          const uint4* src = (const uint4*)((part ? P.q_lo : P.q_hi) +
+                                            (int64_t)(pi >= 0 ? pi / P.n_p : 0) * (DP / 2));
+          const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + a_col + part * (DP / 2);
+#pragma unroll 1
+          for (int c16 = 0; c16 < DP / 2; c16 += 16) {
+            uint32_t v[16];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int j = ch * 8 + e;
-            const float x = (qv && j < d) ? __ldg(qv + j) * 16384.0f : 0.0f;
-            h[e] = split_pack(x, lw[e]);
+            for (int x = 0; x < 4; ++x) {
+              const uint4 w4 = pi >= 0 ? __ldg(src + c16 / 4 + x) : make_uint4(0, 0, 0, 0);
+              v[4 * x] = w4.x;
+              v[4 * x + 1] = w4.y;
+              v[4 * x + 2] = w4.z;
+              v[4 * x + 3] = w4.w;
+            }
+            sm100::tmem_st16(ta + c16, v);
           }
-          const uint32_t o = ch * (kM * 16) + (r >> 3) * 128 + (r & 7) * 16;
-          *(uint4*)(smem + Lo.qhi + o) = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16),
-                                                    h[4] | (h[5] << 16), h[6] | (h[7] << 16));
-          *(uint4*)(smem + Lo.qlo + o) =
-              make_uint4(lw[0] | (lw[1] << 16), lw[2] | (lw[3] << 16), lw[4] | (lw[5] << 16),
-                         lw[6] | (lw[7] << 16));
+          sm100::tmem_st_wait();
         }
-        sm100::fence_proxy_async_smem();
+        sm100::tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full);
         ++u;
@@ -512,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         if (lane == 0) mbar_arrive(&meta_full[ms]);
       }
       __syncwarp();
+      if (warp == kDecWarp0) TRACE(2);
       if (lane == 0) {
         mbar_arrive(&op_full[ob]);
         mbar_arrive(&st_empty[s]);
@@ -533,12 +565,13 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0;
     const int cols = NV / 2;
     for (;;) {
-      const int ab = t & 1, ms = t & (kMeta - 1);
-      sm100::mbar_wait(&acc_full[ab], (t >> 1) & 1);
+      const int ab = t & (kAcc - 1), ms = t & (kMeta - 1);
+      sm100::mbar_wait(&acc_full[ab], (t / kAcc) & 1);
       sm100::mbar_wait(&meta_full[ms], (t / kMeta) & 1);
       const unsigned char* mp = meta(ms);
       const Ctrl c = *(const Ctrl*)mp;
       if (c.list < 0) break;
+      if (warp == kEpiWarp0) TRACE(5);
       const int pi = ((const int*)(mp + Lo.m_qrow))[row];
       if (c.tile == 0) top.init();
       if ((c.tile & 3) == 0) bnd = prune_bound(P, pi);
@@ -547,43 +580,43 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const int* ids = (const int*)(mp + Lo.m_ids);
       const int c0 = half * cols;
 #pragma unroll 1
-      for (int cc = 0; cc < cols; cc += kDrain) {
-        uint32_t r[kDrain];
-        tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
-        float ns[kDrain];
-#pragma unroll
-        for (int e = 0; e < kDrain; e += 4) {
-          const float4 f4 = *(const float4*)(nsc + c0 + cc + e);
-          ns[e] = f4.x;
-          ns[e + 1] = f4.y;
-          ns[e + 2] = f4.z;
-          ns[e + 3] = f4.w;
-        }
+      for (int cc = 0; cc < cols; cc += 32) {
+        uint32_t r[32];
+        sm100::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
         sm100::tmem_ld_wait();
-        // a candidate must beat this half's k-th, the other half's k-th (either
-        // bounds the pair's top-k) and the query's global bound from other lists
-        const float thr =
-            fmaxf(fmaxf(top.s[KMAX - 1], *(volatile float*)&thr_sh[(half ^ 1) * kM + row]), bnd);
-        int cnt = 0;
 #pragma unroll
-        for (int e = 0; e < kDrain; ++e) {
-          const int col = c0 + cc + e;
-          const float res = __fmul_rn(__uint_as_float(r[e]), ns[e]);
-          if (res >= thr) {
-            cand_v[cnt * kEpiThreads + et] = res;
-            cand_c[cnt * kEpiThreads + et] = col;
-            ++cnt;
+        for (int h = 0; h < 32; h += kDrain) {
+          // a candidate must beat this half's k-th, the other half's k-th (either
+          // bounds the pair's top-k) and the query's global bound from other lists
+          const float thr = fmaxf(
+              fmaxf(top.s[KMAX - 1], *(volatile float*)&thr_sh[(half ^ 1) * kM + row]), bnd);
+          int cnt = 0;
+#pragma unroll
+          for (int e = 0; e < kDrain; e += 4) {
+            const float4 f4 = *(const float4*)(nsc + c0 + cc + h + e);
+            const float ns[4] = {f4.x, f4.y, f4.z, f4.w};
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const float res = __fmul_rn(__uint_as_float(r[h + e + x]), ns[x]);
+              if (res >= thr) {
+                cand_v[cnt * kEpiThreads + et] = res;
+                cand_c[cnt * kEpiThreads + et] = c0 + cc + h + e + x;
+                ++cnt;
+              }
+            }
+          }
+          if (__any_sync(kFull, cnt != 0)) {
+            const int mx = __reduce_max_sync(kFull, cnt);
+            for (int i = 0; i < mx; ++i) {
+              if (i < cnt) {
+                const float v = cand_v[i * kEpiThreads + et];
+                const int id = ids[cand_c[i * kEpiThreads + et]];
+                if (top.beats(v, id)) top.insert(v, id);
+              }
+            }
+            *(volatile float*)&thr_sh[half * kM + row] = top.s[KMAX - 1];
           }
         }
-        const int mx = __reduce_max_sync(kFull, cnt);
-        for (int i = 0; i < mx; ++i) {
-          if (i < cnt) {
-            const float v = cand_v[i * kEpiThreads + et];
-            const int id = ids[cand_c[i * kEpiThreads + et]];
-            if (top.beats(v, id)) top.insert(v, id);
-          }
-        }
-        if (mx) *(volatile float*)&thr_sh[half * kM + row] = top.s[KMAX - 1];
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -627,6 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         named_bar(1, kEpiThreads);
       }
       __syncwarp();
+      if (warp == kEpiWarp0) TRACE(6);
       if (lane == 0) mbar_arrive(&meta_empty[ms]);
       ++t;
     }
@@ -739,6 +773,22 @@ __global__ void items_fill_kernel(const int32_t* __restrict__ ntile, const int32
   for (int t = 0; t < nt; ++t) items[S[t] + atomicAdd(&fill[t], 1)] = make_int2(l, t);
 }
 
+// Split each rotated query row once per search into fp16 hi/lo (scaled 2^14),
+// packed 2 per word along K, zero-padded to DP: the A-operand rows of TMEM.
+__global__ void q16_kernel(const float* __restrict__ qrot, int64_t nq, int d, int DP,
+                           uint32_t* __restrict__ hi, uint32_t* __restrict__ lo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int hw = DP / 2;
+  if (i >= nq * hw) return;
+  const int64_t q = i / hw;
+  const int j = (int)(i - q * hw) * 2;
+  uint32_t h0, l0, h1, l1;
+  h0 = split_pack(j < d ? qrot[q * d + j] * 16384.0f : 0.0f, l0);
+  h1 = split_pack(j + 1 < d ? qrot[q * d + j + 1] * 16384.0f : 0.0f, l1);
+  hi[i] = h0 | (h1 << 16);
+  lo[i] = l0 | (l1 << 16);
+}
+
 __global__ void thr_init_kernel(long long* __restrict__ key, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) key[i] = dkey(-INFINITY);
@@ -757,6 +807,7 @@ static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 struct TcScratch {
   int32_t *cnt2, *cursor2, *G, *fill, *counter, *pstart2, *pstart, *ntile, *S, *n_items, *pairs;
   long long* thr_key;
+  uint32_t *q_hi, *q_lo;
   int2* items;
   double* part_s;
   int32_t* part_id;
@@ -765,7 +816,9 @@ struct TcScratch {
   size_t bytes;
 };
 
-static TcScratch carve_tc(void* base, int64_t nq, int n_p, int L, int k) {
+static int pad_dp(int dim) { return (dim + 31) / 32 * 32; }
+
+static TcScratch carve_tc(void* base, int64_t nq, int n_p, int L, int k, int dim) {
   TcScratch S{};
   size_t off = 0;
   char* b = (char*)base;
@@ -791,6 +844,8 @@ static TcScratch carve_tc(void* base, int64_t nq, int n_p, int L, int k) {
   S.n_items = (int32_t*)take(16);
   S.thr_key = (long long*)take(8 * (size_t)nq);
   S.pairs = (int32_t*)take(4 * (size_t)np);
+  S.q_hi = (uint32_t*)take(4 * (size_t)nq * (pad_dp(dim) / 2));
+  S.q_lo = (uint32_t*)take(4 * (size_t)nq * (pad_dp(dim) / 2));
   S.items = (int2*)take(8 * (size_t)max_items);
   S.part_s = (double*)take(8 * (size_t)np * k);
   S.part_id = (int32_t*)take(4 * (size_t)np * k);
@@ -799,7 +854,8 @@ static TcScratch carve_tc(void* base, int64_t nq, int n_p, int L, int k) {
 }
 
 extern "C" size_t ivftq_scan_tc_scratch_bytes(int64_t nq, int n_p, int n_lists, int depth) {
-  return carve_tc(nullptr, nq, n_p, n_lists, depth).bytes + 256;
+  // dim is not known here: size the query rows for the widest supported dim
+  return carve_tc(nullptr, nq, n_p, n_lists, depth, kMaxDim).bytes + 256;
 }
 
 static const size_t kSmemLimit = 227 * 1024;
@@ -808,21 +864,17 @@ static const size_t kSmemLimit = 227 * 1024;
 static int kmax_for(int depth) { return depth <= 10 ? 10 : 32; }
 
 static bool pick_tile(int DP, int W, int C, int kmax, int* nv, int* ns) {
-  const int cands[3][2] = {{128, kNS}, {64, kNS}, {32, kNS}};
-  for (auto& c : cands) {
-    if (make_layout(c[0], c[1], DP, W, C, kmax).total + 1024 <= kSmemLimit) {
-      *nv = c[0];
-      *ns = c[1];
-      return true;
-    }
-  }
-  return false;
+  if (DP > kMaxDim) return false;
+  if (make_layout(kNV, kNS, DP, W, C, kmax).total + 1024 > kSmemLimit) return false;
+  *nv = kNV;
+  *ns = kNS;
+  return true;
 }
 
 extern "C" int ivftq_scan_tc_supported(int dim, int bits, int depth) {
   int fb = field_bits(bits, 1);
   if (fb < 3 || fb > 5 || depth < 1 || depth > 32) return 0;
-  int DP = (dim + 15) / 16 * 16;
+  int DP = pad_dp(dim);
   int W = words_per_vec(dim, fb);
   int nv, ns;
   return pick_tile(DP, W, 1 << fb, kmax_for(depth), &nv, &ns);
@@ -862,7 +914,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  TcScratch S = carve_tc(scratch, nq, n_p, L, depth);
+  TcScratch S = carve_tc(scratch, nq, n_p, L, depth, st->dim);
   int64_t np = nq * n_p;
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(S.cnt2, 0, S.zero_end - (char*)S.cnt2, s));
   unsigned gp = (unsigned)((np + 255) / 256);
@@ -880,7 +932,12 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   if (int e = check_launch("items_fill")) return e;
 
   const int fb = st->field_bits, C = 1 << fb;
-  const int DP = (st->dim + 15) / 16 * 16;
+  const int DP = pad_dp(st->dim);
+  {
+    const int64_t nw = nq * (DP / 2);
+    q16_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(qrot, nq, st->dim, DP, S.q_hi, S.q_lo);
+    if (int e = check_launch("q16")) return e;
+  }
   Params P{};
   const int kmax = kmax_for(depth);
   pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS);
@@ -896,6 +953,15 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   P.part_s = S.part_s;
   P.part_id = S.part_id;
   P.thr_key = S.thr_key;
+  P.q_hi = S.q_hi;
+  P.q_lo = S.q_lo;
+  const char* trace_path = getenv("IVFTQ_TRACE");
+  long long* trace = nullptr;
+  if (trace_path) {
+    cudaMalloc(&trace, sizeof(long long) * 8 * kTraceTiles);
+    cudaMemsetAsync(trace, 0, sizeof(long long) * 8 * kTraceTiles, s);
+  }
+  P.trace = trace;
   P.n_p = n_p;
   P.k = depth;
   P.d = st->dim;
@@ -919,6 +985,23 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   }
 #undef TC_CASE
   if (rc) return rc;
+  if (trace) {
+    static long long h[8 * kTraceTiles];
+    cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    FILE* f = fopen(trace_path, "w");
+    if (f) {
+      fprintf(f, "# NV=%d nbuf=2 tiles: t prod dec_start dec_end mma_start mma_end epi_start epi_end\n", P.NV);
+      for (int t = 0; t < kTraceTiles; ++t) {
+        if (!h[t * 8 + 1]) break;
+        fprintf(f, "%d", t);
+        for (int k = 0; k < 7; ++k) fprintf(f, " %lld", h[t * 8 + k] ? h[t * 8 + k] - h[1] : -1);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+    cudaFree(trace);
+  }
   if (int e = merge_smem_opt_in(depth)) return e;
   launch_merge(S.part_s, S.part_id, nq, n_p * depth, depth, ids_out, scores_out, s);
   return check_launch("merge");

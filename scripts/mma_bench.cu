@@ -1,0 +1,89 @@
+// Microbenchmark: tcgen05.mma kind::f16 issue-to-completion rate for the
+// operand layouts the scan uses (no swizzle vs 128B swizzle, N = 64/128/256).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 \
+//        -I paper_2605_17415_b200/csrc scripts/mma_bench.cu -o /tmp/mma_bench
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "sm100.cuh"
+
+using namespace ivftq;
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t addr, uint32_t sbo) {
+  // K-major, SWIZZLE_128B (layout type 2 at bits 61-63), LBO ignored (1)
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (2ull << 61);
+}
+
+template <int N, bool SW>
+__global__ void bench(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (128 + N) * 128; i += blockDim.x) ((uint16_t*)smem)[i] = 0x3c00;
+  if (tid < 32) sm100::tmem_alloc(&tslot, 256);
+  if (tid == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::mbar_fence_init();
+  }
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t a = sm100::smem_u32(smem), b = a + 128 * 128 * 2;
+  const uint32_t idesc = sm100::idesc_f16_f32(128, N);
+  if (tid == 0) {
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int s = 0; s < 8; ++s) {  // K = 128 in 8 steps
+        uint64_t ad, bd;
+        if (SW) {
+          ad = desc_sw128(a + (s >> 2) * 128 * 128 + (s & 3) * 32, 1024);
+          bd = desc_sw128(b + (s >> 2) * N * 128 + (s & 3) * 32, 1024);
+        } else {
+          ad = sm100::smem_desc(a + s * 2 * 128 * 16, 128 * 16, 128);
+          bd = sm100::smem_desc(b + s * 2 * N * 16, N * 16, 128);
+        }
+        sm100::mma_f16(tmem, ad, bd, idesc, (it | s) ? 1u : 0u);
+      }
+    }
+    sm100::mma_commit(&bar);
+    sm100::mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) sm100::tmem_dealloc(tmem, 256);
+}
+
+template <int N, bool SW>
+void run(const char* name) {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  int iters = 2000;
+  size_t smem = (128 + N) * 128 * 2 + 1024;
+  cudaFuncSetAttribute(bench<N, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bench<N, SW><<<148, 128, smem>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double cyc = (double)h[0] / (iters * 8);
+  double flops = 2.0 * 128 * N * 16 / cyc;  // per SM per cycle
+  printf("%-14s N=%3d: %7.1f cycles/MMA  %7.0f flop/cyc/SM  (%s)\n", name, N, cyc, flops,
+         cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+int main() {
+  run<64, false>("noswizzle");
+  run<128, false>("noswizzle");
+  run<256, false>("noswizzle");
+  run<64, true>("swizzle128");
+  run<128, true>("swizzle128");
+  run<256, true>("swizzle128");
+  return 0;
+}
