@@ -105,7 +105,7 @@ struct Layout {
 __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x + a - 1) & ~(a - 1); }
 
 // candidate-buffer entries per epilogue thread: a drain window, or a whole
-// top-K list when the two column halves merge
+// top-K list when the two column halves merge at the end of an item
 __host__ __device__ inline int cand_entries(int kmax) { return kmax > kDrain ? kmax : kDrain; }
 
 __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int C, int KMAX) {
@@ -162,19 +162,19 @@ struct RegTopK {
   __device__ __forceinline__ bool beats(float v, int id) const {
     return v > s[K - 1] || (v == s[K - 1] && id < i[K - 1]);
   }
-  // precondition: beats(v, id)
+  // precondition: beats(v, id). Branch-free and chain-free: every position
+  // compares against the old list at once (g is monotone in p because the
+  // list is sorted), so the insert is ~2K independent selects, depth ~3.
   __device__ __forceinline__ void insert(float v, int id) {
-    bool placed = false;
+    bool g[K];
+#pragma unroll
+    for (int p = 0; p < K; ++p) g[p] = v > s[p] || (v == s[p] && id < i[p]);
 #pragma unroll
     for (int p = K - 1; p > 0; --p) {
-      bool up = !placed && (v > s[p - 1] || (v == s[p - 1] && id < i[p - 1]));
-      float ns = up ? s[p - 1] : (placed ? s[p] : v);
-      int ni = up ? i[p - 1] : (placed ? i[p] : id);
-      s[p] = ns;
-      i[p] = ni;
-      placed = placed || !up;
+      s[p] = g[p] ? (g[p - 1] ? s[p - 1] : v) : s[p];
+      i[p] = g[p] ? (g[p - 1] ? i[p - 1] : id) : i[p];
     }
-    if (!placed) { s[0] = v; i[0] = id; }
+    if (g[0]) { s[0] = v; i[0] = id; }
   }
 };
 
@@ -572,6 +572,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const Ctrl c = *(const Ctrl*)mp;
       if (c.list < 0) break;
       if (warp == kEpiWarp0) TRACE(5);
+      if (P.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarp0 && t < (uint32_t)kTraceTiles)
+        P.trace[t * 8 + 7] = c.tile | (c.ntiles << 12) | ((long long)c.nqt << 24);
       const int pi = ((const int*)(mp + Lo.m_qrow))[row];
       if (c.tile == 0) top.init();
       if ((c.tile & 3) == 0) bnd = prune_bound(P, pi);
@@ -584,12 +586,13 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         uint32_t r[32];
         sm100::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
         sm100::tmem_ld_wait();
+        // a candidate must beat this half's k-th, the other half's k-th (either
+        // bounds the pair's top-k) and the query's global bound from other lists
 #pragma unroll
         for (int h = 0; h < 32; h += kDrain) {
-          // a candidate must beat this half's k-th, the other half's k-th (either
-          // bounds the pair's top-k) and the query's global bound from other lists
           const float thr = fmaxf(
               fmaxf(top.s[KMAX - 1], *(volatile float*)&thr_sh[(half ^ 1) * kM + row]), bnd);
+          // survivors of this window go to the thread's own buffer column
           int cnt = 0;
 #pragma unroll
           for (int e = 0; e < kDrain; e += 4) {
@@ -598,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
               const float res = __fmul_rn(__uint_as_float(r[h + e + x]), ns[x]);
-              if (res >= thr) {
+              if (res >= thr) {  // NaN (padding) never passes
                 cand_v[cnt * kEpiThreads + et] = res;
                 cand_c[cnt * kEpiThreads + et] = c0 + cc + h + e + x;
                 ++cnt;
@@ -996,6 +999,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
         if (!h[t * 8 + 1]) break;
         fprintf(f, "%d", t);
         for (int k = 0; k < 7; ++k) fprintf(f, " %lld", h[t * 8 + k] ? h[t * 8 + k] - h[1] : -1);
+        fprintf(f, " %lld %lld %lld", h[t * 8 + 7] & 4095, (h[t * 8 + 7] >> 12) & 4095, h[t * 8 + 7] >> 24);
         fprintf(f, "\n");
       }
       fclose(f);
