@@ -169,6 +169,10 @@ int ivftq_scan_topk_tc(const ivftq_store* store, const int32_t* probe, const dou
                        const float* qrot, const double* levels, int64_t nq, int n_p,
                        int depth, int64_t* ids_out, double* scores_out, void* scratch,
                        size_t scratch_bytes, void* stream);
+/* Instrumentation: bracket the tensor-core scan kernel with CUDA events on its
+ * stream; ivftq_last_scan_kernel_ms() syncs and returns the last duration. */
+int ivftq_set_kernel_timing(int on);
+double ivftq_last_scan_kernel_ms(void);
 /* Exact re-score of the top-depth candidates against the raw f32 store and
  * re-order to top-k (index.py:470-473). */
 int ivftq_rerank(const float* raw, const double* qn, const int64_t* cand_ids,

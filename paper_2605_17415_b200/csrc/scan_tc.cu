@@ -805,6 +805,27 @@ using namespace ivftq::tc;
 
 static int g_num_sms = 0;
 
+// Optional device timing of the scan kernel alone (bench roofline evidence).
+static bool g_time_kernel = false;
+static cudaEvent_t g_ev[2] = {nullptr, nullptr};
+
+extern "C" int ivftq_set_kernel_timing(int on) {
+  g_time_kernel = on != 0;
+  if (g_time_kernel && !g_ev[0]) {
+    IVFTQ_CHECK_CUDA(cudaEventCreate(&g_ev[0]));
+    IVFTQ_CHECK_CUDA(cudaEventCreate(&g_ev[1]));
+  }
+  return 0;
+}
+
+extern "C" double ivftq_last_scan_kernel_ms(void) {
+  if (!g_ev[0]) return -1.0;
+  float ms = -1.f;
+  if (cudaEventSynchronize(g_ev[1]) != cudaSuccess) return -1.0;
+  if (cudaEventElapsedTime(&ms, g_ev[0], g_ev[1]) != cudaSuccess) return -1.0;
+  return ms;
+}
+
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct TcScratch {
@@ -892,7 +913,9 @@ static int launch_tc(const Params& P, size_t smem, int grid, cudaStream_t s) {
     set_error("scan_tc: smem %zu rejected: %s", smem, cudaGetErrorString(e));
     return IVFTQ_ERR_UNSUPPORTED;
   }
+  if (g_time_kernel) cudaEventRecord(g_ev[0], s);
   fn<<<grid, kThreads, smem, s>>>(P);
+  if (g_time_kernel) cudaEventRecord(g_ev[1], s);
   return check_launch("scan_tc");
 }
 

@@ -43,6 +43,229 @@ select_topn_kernel(const double* __restrict__ scores, int cols, int n,
   }
 }
 
+// Small n (every realistic nprobe): one warp per row keeps the row's best n
+// as a sorted queue in registers, 32*S positions (position s*32+lane in
+// slot s of that lane). Columns stream through in ascending order 32 at a
+// time; a column enters only if it beats the current n-th entry, so after the
+// first few chunks almost every column is rejected by one compare + ballot.
+// Since columns arrive in ascending id order, an entry equal in value to a
+// queued one belongs after it: the insert position is the count of queued
+// keys >= its key, which reproduces (value desc, column asc) exactly.
+// Values are compared as order-preserving int64 keys (-0.0 folded onto +0.0,
+// NaN below -inf, matching a stable argsort of -scores).
+__device__ __forceinline__ long long order_key(double x) {
+  if (x == 0.0) x = 0.0;
+  long long b = __double_as_longlong(x);
+  if (x != x) return LLONG_MIN;
+  return b >= 0 ? b : (b ^ 0x7fffffffffffffffLL);
+}
+__device__ __forceinline__ double key_value(long long k) {
+  return __longlong_as_double(k >= 0 ? k : (k ^ 0x7fffffffffffffffLL));
+}
+
+template <int S>
+__device__ void warp_queue_select(const double* __restrict__ row, int cols, int n,
+                                  int32_t* __restrict__ io, double* __restrict__ vo) {
+  const int lane = threadIdx.x & 31;
+  long long qk[S];
+  int qi[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) { qk[s] = LLONG_MIN; qi[s] = -1; }
+  int cnt = 0;                      // filled positions
+  long long thr = LLONG_MIN;        // key at position n-1 once full
+  const int tl = (n - 1) & 31, ts = (n - 1) >> 5;
+  constexpr int kPre = 4;           // chunks loaded ahead
+  for (int base = 0; base < cols; base += 32 * kPre) {
+    double v[kPre];
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const int c = base + u * 32 + lane;
+      v[u] = c < cols ? __ldg(row + c) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPre; ++u) {
+      const int c = base + u * 32 + lane;
+      const long long key = order_key(v[u]);
+      unsigned m = __ballot_sync(kFull, c < cols && (cnt < n || key > thr));
+      while (m) {
+        const int src = __ffs(m) - 1;
+        m &= m - 1;
+        const long long k = __shfl_sync(kFull, key, src);
+        if (cnt == n && !(k > thr)) continue;   // threshold rose meanwhile
+        int p = 0;
+#pragma unroll
+        for (int s = 0; s < S; ++s)
+          p += __popc(__ballot_sync(kFull, (s * 32 + lane) < cnt && qk[s] >= k));
+        // shift positions >= p one place later; the entry at n-1 falls off
+        long long rk[S];
+        int ri[S];
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+          rk[s] = __shfl_sync(kFull, qk[s], (lane + 31) & 31);
+          ri[s] = __shfl_sync(kFull, qi[s], (lane + 31) & 31);
+        }
+#pragma unroll
+        for (int s = S - 1; s >= 0; --s) {
+          const int pos = s * 32 + lane;
+          long long pk = rk[s];
+          int pi = ri[s];
+          if (lane == 0) {
+            pk = s > 0 ? rk[s > 0 ? s - 1 : 0] : LLONG_MIN;
+            pi = s > 0 ? ri[s > 0 ? s - 1 : 0] : -1;
+          }
+          if (pos > p) { qk[s] = pk; qi[s] = pi; }
+          else if (pos == p) { qk[s] = k; qi[s] = base + u * 32 + src; }
+        }
+        cnt = min(cnt + 1, n);
+        if (cnt == n) {
+          long long t = qk[0];
+#pragma unroll
+          for (int s = 1; s < S; ++s) if (s == ts) t = qk[s];
+          thr = __shfl_sync(kFull, t, tl);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int pos = s * 32 + lane;
+    if (pos < n) {
+      const bool ok = pos < cnt;
+      io[pos] = ok ? qi[s] : -1;
+      vo[pos] = ok ? key_value(qk[s]) : -INFINITY;
+    }
+  }
+}
+
+// Fast path, one warp per row, three passes over the (L1/L2-resident) row:
+//   1. min / max;
+//   2. a 256-bin histogram of the linear map (v - min) * 256 / (max - min),
+//      monotone in v, so the bin b holding the n-th best value bounds the
+//      selection: every value in bins > b is in, every value in bins < b out;
+//   3. compact the values in bins >= b (normally n plus a few) into shared
+//      memory and give each its exact rank (count of better candidates under
+//      value desc / column asc); ranks < n are the answer.
+// Rows the map cannot split (NaN, infinities, all-equal, or a boundary bin so
+// crowded that the candidates overflow) take the warp-queue path above, which
+// is exact for any input.
+constexpr int kSelBins = 256;
+template <int S>
+__global__ void __launch_bounds__(256)
+select_warp_kernel(const double* __restrict__ scores, int64_t rows, int cols, int n,
+                   int32_t* __restrict__ idx_out, double* __restrict__ val_out) {
+  constexpr int CAP = 32 * S + 64;
+  constexpr int kWarps = 8;
+  __shared__ unsigned hist_all[kWarps][kSelBins];
+  __shared__ long long ck_all[kWarps][CAP];
+  __shared__ int ci_all[kWarps][CAP];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * kWarps + warp;
+  if (r >= rows) return;
+  const double* row = scores + r * cols;
+  int32_t* io = idx_out + r * n;
+  double* vo = val_out + r * n;
+  unsigned* hist = hist_all[warp];
+  long long* ck = ck_all[warp];
+  int* ci = ci_all[warp];
+
+  double mn = INFINITY, mx = -INFINITY;
+  bool nan = false;
+  for (int c = lane; c < cols; c += 32) {
+    const double v = __ldg(row + c);
+    nan |= v != v;
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = fmin(mn, __shfl_xor_sync(kFull, mn, o));
+    mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+  }
+  const double span = mx - mn;
+  if (__any_sync(kFull, nan) || !(span > 0.0) || !(span < INFINITY)) {
+    warp_queue_select<S>(row, cols, n, io, vo);
+    return;
+  }
+  const double scale = (double)kSelBins / span;
+  auto bin_of = [&](double v) { return min(kSelBins - 1, (int)((v - mn) * scale)); };
+#pragma unroll
+  for (int i = 0; i < kSelBins / 32; ++i) hist[i * 32 + lane] = 0;
+  __syncwarp();
+  for (int c = lane; c < cols; c += 32) atomicAdd(&hist[bin_of(__ldg(row + c))], 1u);
+  __syncwarp();
+  // lane l owns bins [kSelBins-8(l+1), kSelBins-8l), i.e. lane 0 the top bins
+  unsigned own[kSelBins / 32];
+  unsigned tot = 0;
+#pragma unroll
+  for (int i = 0; i < kSelBins / 32; ++i) {
+    own[i] = hist[kSelBins - 1 - (lane * (kSelBins / 32) + i)];
+    tot += own[i];
+  }
+  unsigned incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const unsigned excl = incl - tot;
+  const int owner = __ffs(__ballot_sync(kFull, incl >= (unsigned)n)) - 1;
+  int bsel = 0;
+  if (lane == owner) {
+    unsigned acc = excl;
+#pragma unroll
+    for (int i = 0; i < kSelBins / 32; ++i) {
+      acc += own[i];
+      if (acc >= (unsigned)n) { bsel = kSelBins - 1 - (lane * (kSelBins / 32) + i); break; }
+    }
+  }
+  const int b = __shfl_sync(kFull, bsel, owner);
+  const unsigned total = __shfl_sync(kFull, incl, owner);  // upper bound on candidates
+  (void)total;
+  int c_n = 0;
+  for (int base = 0; base < cols; base += 32) {
+    const int c = base + lane;
+    double v = 0.0;
+    bool in = false;
+    if (c < cols) {
+      v = __ldg(row + c);
+      in = bin_of(v) >= b;
+    }
+    const unsigned m = __ballot_sync(kFull, in);
+    const int at = c_n + __popc(m & ((1u << lane) - 1u));
+    if (in && at < CAP) { ck[at] = order_key(v); ci[at] = c; }
+    c_n += __popc(m);
+  }
+  if (c_n > CAP) {
+    warp_queue_select<S>(row, cols, n, io, vo);
+    return;
+  }
+  __syncwarp();
+  constexpr int PER = (CAP + 31) / 32;
+  long long mk[PER];
+  int mi[PER], rank[PER];
+#pragma unroll
+  for (int t = 0; t < PER; ++t) {
+    const int i = t * 32 + lane;
+    mk[t] = i < c_n ? ck[i] : LLONG_MIN;
+    mi[t] = i < c_n ? ci[i] : INT_MAX;
+    rank[t] = 0;
+  }
+  for (int j = 0; j < c_n; ++j) {
+    const long long kj = ck[j];
+    const int ij = ci[j];
+#pragma unroll
+    for (int t = 0; t < PER; ++t) rank[t] += (kj > mk[t]) || (kj == mk[t] && ij < mi[t]);
+  }
+#pragma unroll
+  for (int t = 0; t < PER; ++t) {
+    const int i = t * 32 + lane;
+    if (i < c_n && rank[t] < n) {
+      io[rank[t]] = mi[t];
+      vo[rank[t]] = key_value(mk[t]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // LUT list scan. Block = (query q, probe split). The block builds the query's
 // LUT lut[j][c] = f32(qrot_j * T32[c]) in shared memory (field c is the
@@ -247,6 +470,17 @@ extern "C" int ivftq_select_topn(const double* scores, int64_t rows, int cols, i
     return IVFTQ_ERR_ARG;
   }
   if (rows == 0) return 0;
+  if (n <= 128) {
+    const unsigned blocks = (unsigned)((rows + 7) / 8);
+    auto s = (cudaStream_t)stream;
+    if (n <= 32)
+      select_warp_kernel<1><<<blocks, 256, 0, s>>>(scores, rows, cols, n, idx_out, val_out);
+    else if (n <= 64)
+      select_warp_kernel<2><<<blocks, 256, 0, s>>>(scores, rows, cols, n, idx_out, val_out);
+    else
+      select_warp_kernel<4><<<blocks, 256, 0, s>>>(scores, rows, cols, n, idx_out, val_out);
+    return check_launch("select_warp");
+  }
   size_t sm = BlockTopK::bytes(topk_cap(n, 128));
   if (int e = smem_opt_in((const void*)select_topn_kernel, sm)) return e;
   select_topn_kernel<<<(unsigned)rows, 128, sm, (cudaStream_t)stream>>>(scores, cols, n,

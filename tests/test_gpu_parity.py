@@ -208,6 +208,38 @@ def test_exact_topk_gpu_matches_reference(golden):
         np.testing.assert_array_equal(t.ids, g["truth10"])
 
 
+@pytest.mark.parametrize("cols,n", [(1, 1), (7, 3), (64, 64), (1024, 1), (1024, 32),
+                                    (1024, 33), (1024, 64), (1000, 100), (4096, 128),
+                                    (4096, 129), (300, 257)])
+def test_select_topn_stable_order(cols, n):
+    """Per-row top-n must equal a stable argsort of -scores (index.py:438),
+    including exact ties (lower column first), -0.0 == 0.0 and NaN last."""
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+
+    rng = np.random.default_rng(cols * 1000 + n)
+    rows = 37
+    S = rng.integers(-8, 8, size=(rows, cols)).astype(np.float64) / 8.0  # many ties
+    S[0] = rng.standard_normal(cols)
+    if cols > 4:
+        S[1, :: 3] = -0.0
+        S[1, 1:: 3] = 0.0
+        if n <= 128:  # the warp-queue path orders NaN last like argsort
+            S[2, ::5] = np.nan
+    S[3] = 0.25
+    dS = torch.from_numpy(S).cuda()
+    idx = torch.empty((rows, n), dtype=torch.int32, device="cuda")
+    val = torch.empty((rows, n), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.lib().ivftq_select_topn(dS.data_ptr(), rows, cols, n, idx.data_ptr(),
+                                             val.data_ptr(), None), "select_topn")
+    torch.cuda.synchronize()
+    want = np.argsort(-S, axis=1, kind="stable")[:, :n]
+    np.testing.assert_array_equal(idx.cpu().numpy(), want)
+    wv = np.take_along_axis(S, want, axis=1)
+    np.testing.assert_array_equal(val.cpu().numpy(), wv)
+
+
 class TestEdgeCases:
     def test_errors_and_warnings(self, golden):
         g = golden("d32_b4_L16_raw")
