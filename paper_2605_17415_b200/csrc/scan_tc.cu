@@ -34,6 +34,7 @@
 // same order as the reference's own f32 sgemm. The residual term is then
 // D * (2^-(eT+14) * f32(||r||)), the candidate score coarse + (double)res.
 #include <climits>
+#include <string>
 #include <cstdlib>
 #include <cstdio>
 
@@ -56,7 +57,9 @@ constexpr int kDecWarp0 = 2;     // decoder warps 2..9
 constexpr int kDecWarps = 8;
 constexpr int kEpiWarp0 = 10;    // epilogue warps 10..17
 constexpr int kEpiWarps = 8;
-constexpr int kThreads = 32 * (kEpiWarp0 + kEpiWarps);  // 576
+constexpr int kSchedWarp = kEpiWarp0 + kEpiWarps;  // 18: item scheduler
+constexpr int kThreads = 32 * (kSchedWarp + 1);      // 608
+constexpr int kItemSlots = 2;    // item-record ring (scheduler -> producer)
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
 constexpr int kNS = 4;           // stage ring depth (power of two)
@@ -83,6 +86,8 @@ struct Params {
   const uint32_t* q_hi;    // [nq][DP/2] rotated query rows, fp16 hi halves (x 2^14), packed pairs
   const uint32_t* q_lo;    // [nq][DP/2] matching lo halves
   int n_p, k, d, DP, NV, NS;
+  int nA;           // A-operand buffers in TMEM (2 when they fit: next item's
+                    // queries are written while the current item's MMAs run)
   float t_scale;    // 2^eT
   float inv_scale;  // 2^-(eT+14)
 };
@@ -97,7 +102,21 @@ struct Ctrl {
   int pad[3];
 };
 
+// one work item as the scheduler warp prepares it for the producer
+struct ItemRec {
+  int list;    // -1 = stop
+  int nqt;
+  int size;
+  int ntiles;
+  long long off;
+  long long pad;
+  int prow[kM];       // pair index of each query row (-1 = padding)
+  float bnd[kM];      // residual-space pruning bound at fetch time
+  double cs[kM];      // coarse score of each pair
+};
+
 struct Layout {
+  uint32_t items, item_bytes;
   uint32_t bhi[2], blo[2], stage, stage_bytes, st_codes, st_norms, st_ids, st_ctrl,
       st_qrow, meta0, meta_bytes, m_nsc, m_ids, m_qrow, cand, tab, thr, bars, misc, total;
 };
@@ -106,7 +125,6 @@ __host__ __device__ inline uint32_t align_up(uint32_t x, uint32_t a) { return (x
 
 // candidate-buffer entries per epilogue thread: a drain window, or a whole
 // top-K list when the two column halves merge at the end of an item
-__host__ __device__ inline int cand_entries(int kmax) { return kmax > kDrain ? kmax : kDrain; }
 
 __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int C, int KMAX) {
   Layout L{};
@@ -126,17 +144,19 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.st_ids = L.st_norms + align_up(NV * 2, 128);
   L.st_ctrl = L.st_ids + align_up(NV * 4, 128);
   L.st_qrow = L.st_ctrl + 128;
-  L.stage_bytes = L.st_qrow + kM * 4;
+  L.stage_bytes = L.st_qrow + kM * 8;  // query rows (int) + pruning bounds (float)
   L.stage = take(L.stage_bytes * NS);
   // per-accumulator-buffer epilogue record: ctrl | nsc | ids | qrow
   L.m_nsc = 128;
   L.m_ids = L.m_nsc + align_up(NV * 4, 128);
   L.m_qrow = L.m_ids + align_up(NV * 4, 128);
-  L.meta_bytes = align_up(L.m_qrow + kM * 4, 128);
+  L.meta_bytes = align_up(L.m_qrow + kM * 8, 128);
   L.meta0 = take(L.meta_bytes * kMeta);
-  L.cand = take(cand_entries(KMAX) * kEpiThreads * 8);
+  L.cand = 0;
   L.tab = take(C * 4);
-  L.thr = take(2 * kM * 4);
+  L.thr = take(2 * kM * 8);  // per half and row: (item tag << 32) | f32 k-th score
+  L.item_bytes = align_up(sizeof(ItemRec), 128);
+  L.items = take(L.item_bytes * kItemSlots);
   L.bars = take(8 * 48);
   L.misc = take(64);
   L.total = off;
@@ -150,31 +170,55 @@ __device__ __forceinline__ uint32_t split_pack(float x, uint32_t& lo) {
   return (uint32_t)__half_as_ushort(h);
 }
 
-// Register top-K with the library key (score desc, id asc).
+// Register top-K over 64-bit keys that encode the library order (score desc,
+// id asc): high word = order-preserving bits of the f32 residual term (one
+// pair has one coarse score, so the f64 candidate score is monotone in it;
+// -0.0 is folded onto +0.0 so the tie goes to the id), low word = ~id. Key 0
+// is "empty" and sorts below every real candidate (NaN never reaches insert).
+__device__ __forceinline__ uint64_t cand_key(float v, int id) {
+  uint32_t b = __float_as_uint(v + 0.0f);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return ((uint64_t)b << 32) | (uint32_t)~(uint32_t)id;
+}
+__device__ __forceinline__ float key_score(uint64_t k) {
+  const uint32_t o = (uint32_t)(k >> 32);
+  return __uint_as_float((o & 0x80000000u) ? (o & 0x7fffffffu) : ~o);
+}
+__device__ __forceinline__ int key_id(uint64_t k) { return (int)~(uint32_t)k; }
+
+// v[j] for a lane-varying j without local memory: a 4-level select tree
+__device__ __forceinline__ float pick16(const float (&v)[16], int j) {
+  float a[8], b[4], c[2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = (j & 2) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) c[i] = (j & 4) ? b[2 * i + 1] : b[2 * i];
+  return (j & 8) ? c[1] : c[0];
+}
+
 template <int K>
 struct RegTopK {
-  float s[K];
-  int i[K];
+  uint64_t k[K];
   __device__ __forceinline__ void init() {
 #pragma unroll
-    for (int p = 0; p < K; ++p) { s[p] = -INFINITY; i[p] = INT_MAX; }
+    for (int p = 0; p < K; ++p) k[p] = 0;
   }
-  __device__ __forceinline__ bool beats(float v, int id) const {
-    return v > s[K - 1] || (v == s[K - 1] && id < i[K - 1]);
+  __device__ __forceinline__ float kth() const {
+    return k[K - 1] ? key_score(k[K - 1]) : -INFINITY;
   }
-  // precondition: beats(v, id). Branch-free and chain-free: every position
-  // compares against the old list at once (g is monotone in p because the
-  // list is sorted), so the insert is ~2K independent selects, depth ~3.
-  __device__ __forceinline__ void insert(float v, int id) {
+  // Branch-free and chain-free: every position compares against the old list
+  // at once (g is monotone in p because the list is sorted), so an insert is
+  // K compares + 2K selects at depth ~3; a key that does not beat k[K-1]
+  // (including 0) leaves the list unchanged, so callers need no branch.
+  __device__ __forceinline__ void insert(uint64_t key) {
     bool g[K];
 #pragma unroll
-    for (int p = 0; p < K; ++p) g[p] = v > s[p] || (v == s[p] && id < i[p]);
+    for (int p = 0; p < K; ++p) g[p] = key > k[p];
 #pragma unroll
-    for (int p = K - 1; p > 0; --p) {
-      s[p] = g[p] ? (g[p - 1] ? s[p - 1] : v) : s[p];
-      i[p] = g[p] ? (g[p - 1] ? i[p - 1] : id) : i[p];
-    }
-    if (g[0]) { s[0] = v; i[0] = id; }
+    for (int p = K - 1; p > 0; --p) k[p] = g[p] ? (g[p - 1] ? k[p - 1] : key) : k[p];
+    k[0] = g[0] ? key : k[0];
   }
 };
 
@@ -185,6 +229,20 @@ constexpr int kTraceTiles = 4096;
   do {                                                                           \
     if (P.trace && blockIdx.x == 0 && lane == 0 && t < (uint32_t)kTraceTiles)    \
       P.trace[t * 8 + (slot)] = clock64();                                       \
+  } while (0)
+// epilogue-internal timeline (warp kEpiWarp0, lane 0 of CTA 0)
+#define ETRACE(slot, val)                                                        \
+  do {                                                                           \
+    if (P.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarp0 &&          \
+        t < (uint32_t)kTraceTiles)                                               \
+      P.trace[8 * kTraceTiles + t * 8 + (slot)] = (val);                         \
+  } while (0)
+// decoder-internal timeline (warp kDecWarp0, lane 0 of CTA 0)
+#define DTRACE(slot)                                                             \
+  do {                                                                           \
+    if (P.trace && blockIdx.x == 0 && lane == 0 && warp == kDecWarp0 &&          \
+        t < (uint32_t)kTraceTiles)                                               \
+      P.trace[16 * kTraceTiles + t * 8 + (slot)] = clock64();                    \
   } while (0)
 
 // f64 <-> int64 key preserving order, so atomicMax works on scores
@@ -201,12 +259,10 @@ __device__ __forceinline__ double dkey_inv(long long k) {
 // score) strictly -- the 1e-12 margin dominates the f64 rounding of
 // coarse + res and nextafterf undoes the f32 conversion's rounding -- so it
 // can never enter the query's top-k, ties included.
-__device__ __forceinline__ float prune_bound(const Params& P, int pi) {
-  if (pi < 0) return -INFINITY;
-  const long long k = *(volatile const long long*)&P.thr_key[pi / P.n_p];
-  const double thr = dkey_inv(k);
+__device__ __forceinline__ float prune_bound(long long key, double coarse) {
+  const double thr = dkey_inv(key);
   if (!(thr > -INFINITY)) return -INFINITY;
-  const float b = (float)(thr - P.coarse[pi] - 1e-12);
+  const float b = (float)(thr - coarse - 1e-12);
   return nextafterf(b, -INFINITY);
 }
 
@@ -243,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   // TMEM columns: kAcc accumulators of NV columns, then the A operand
   // (Qhi, Qlo: DP/2 columns each)
   const uint32_t a_col = kAcc * NV;
-  const uint32_t need = a_col + DP;
+  const uint32_t need = a_col + P.nA * DP;
   const uint32_t tmem_cols = need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
   const Layout Lo = make_layout(NV, NS, DP, W, C, KMAX);
   uint32_t* tab = (uint32_t*)(smem + Lo.tab);
@@ -254,12 +310,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   uint64_t* op_empty = bars + 18;      // [2] MMA commit -> decoders
   uint64_t* acc_full = bars + 36;      // [kAcc] MMA commit -> epilogue
   uint64_t* acc_empty = bars + 40;     // [kAcc] epilogue -> MMA
-  uint64_t* a_full = bars + 24;        // decoders -> MMA (A operand built)
-  uint64_t* a_empty = bars + 25;       // MMA commit -> decoders (A operand free)
+  uint64_t* a_full = bars + 20;        // [nA] decoders -> MMA (A operand built)
+  uint64_t* a_empty = bars + 22;       // [nA] MMA commit -> decoders (A operand free)
   uint64_t* meta_full = bars + 26;     // [kMeta] decoders -> MMA/epilogue (tile record)
   uint64_t* meta_empty = bars + 30;    // [kMeta] epilogue -> decoders
+  uint64_t* it_full = bars + 34;       // [kItemSlots] scheduler -> producer
+  uint64_t* it_empty = bars + 44;      // [kItemSlots] producer -> scheduler
   uint32_t* tmem_slot = (uint32_t*)(smem + Lo.misc);
-  for (int i = tid; i < 2 * kM; i += kThreads) ((float*)(smem + Lo.thr))[i] = -INFINITY;
+  for (int i = tid; i < 2 * kM; i += kThreads) ((unsigned long long*)(smem + Lo.thr))[i] = 0ull;
   auto meta = [&](int m) { return smem + Lo.meta0 + (uint32_t)m * Lo.meta_bytes; };
   auto stage = [&](int s) { return smem + Lo.stage + (uint32_t)s * Lo.stage_bytes; };
 
@@ -287,8 +345,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       sm100::mbar_init(&meta_full[m], kDecWarps);
       sm100::mbar_init(&meta_empty[m], kEpiWarps);
     }
-    sm100::mbar_init(a_full, kDecWarps);
-    sm100::mbar_init(a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&a_full[b], kDecWarps);
+      sm100::mbar_init(&a_empty[b], 1);
+    }
+    for (int b = 0; b < kItemSlots; ++b) {
+      sm100::mbar_init(&it_full[b], 1);
+      sm100::mbar_init(&it_empty[b], 1);
+    }
     sm100::mbar_fence_init();
   }
   sm100::fence_proxy_async_smem();
@@ -299,13 +363,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
 
   if (warp == kProdWarp) {
     // ================= producer =================================================
-    const int n_items = *P.n_items;
-    uint32_t t = 0;
+    // Per tile: query rows + fresh pruning bounds into the stage slot, then one
+    // lane issues the TMA bulk copies. Item metadata arrives ready-made from
+    // the scheduler warp; the bounds' global loads for tile i+1 are issued
+    // during tile i, so no global latency sits on this warp's per-tile path.
+    uint32_t t = 0, j = 0;
     for (;;) {
-      int item = 0;
-      if (lane == 0) item = atomicAdd(P.counter, 1);
-      item = __shfl_sync(kFull, item, 0);
-      if (item >= n_items) {
+      const int slot = j % kItemSlots;
+      sm100::mbar_wait(&it_full[slot], (j / kItemSlots) & 1);
+      const ItemRec* rec = (const ItemRec*)(smem + Lo.items + slot * Lo.item_bytes);
+      const int l = rec->list;
+      if (l < 0) {
         const int s = t % NS;
         if (t >= (uint32_t)NS) sm100::mbar_wait(&st_empty[s], ((t / NS) - 1) & 1);
         if (lane == 0) {
@@ -315,29 +383,43 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         }
         break;
       }
-      const int2 it = P.items[item];
-      const int l = it.x;
-      const int pbase = P.pstart[l] + it.y * kM;
-      const int nqt = min(kM, P.pstart[l + 1] - pbase);
-      const int size = P.st.list_size[l];
-      const int64_t off = P.st.list_offset[l];
-      const int ntiles = (size + NV - 1) / NV;
-      if (ntiles == 0) {  // empty list: every probing query gets -inf padding
-        for (int r = lane; r < nqt; r += 32) {
-          const int64_t ob = (int64_t)P.pair_idx[pbase + r] * P.k;
-          for (int p = 0; p < P.k; ++p) {
-            P.part_s[ob + p] = -INFINITY;
-            P.part_id[ob + p] = INT_MAX;
-          }
-        }
-        continue;
+      const int nqt = rec->nqt, size = rec->size, ntiles = rec->ntiles;
+      const int64_t off = rec->off;
+      int prow[kM / 32];
+      double pcs[kM / 32];
+      float pb[kM / 32];
+#pragma unroll
+      for (int q = 0; q < kM / 32; ++q) {
+        prow[q] = rec->prow[q * 32 + lane];
+        pcs[q] = rec->cs[q * 32 + lane];
+        pb[q] = rec->bnd[q * 32 + lane];
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&it_empty[slot]);
+      ++j;
+      long long kq[kM / 32];
       for (int i = 0; i < ntiles; ++i, ++t) {
+        if (i > 0) {
+#pragma unroll
+          for (int q = 0; q < kM / 32; ++q)
+            pb[q] = prow[q] >= 0 ? fmaxf(pb[q], prune_bound(kq[q], pcs[q])) : -INFINITY;
+        }
+        if (i + 1 < ntiles) {  // bounds for the next tile: in flight during this one
+#pragma unroll
+          for (int q = 0; q < kM / 32; ++q)
+            kq[q] = prow[q] >= 0 ? *(volatile const long long*)&P.thr_key[prow[q] / P.n_p]
+                                 : LLONG_MIN;
+        }
         const int s = t % NS;
         if (t >= (uint32_t)NS) sm100::mbar_wait(&st_empty[s], ((t / NS) - 1) & 1);
         unsigned char* sp = stage(s);
         int* qrow = (int*)(sp + Lo.st_qrow);
-        for (int r = lane; r < kM; r += 32) qrow[r] = r < nqt ? P.pair_idx[pbase + r] : -1;
+        float* qb = (float*)(qrow + kM);
+#pragma unroll
+        for (int q = 0; q < kM / 32; ++q) {
+          qrow[q * 32 + lane] = prow[q];
+          qb[q * 32 + lane] = pb[q];
+        }
         if (lane == 0) {
           Ctrl* c = (Ctrl*)(sp + Lo.st_ctrl);
           c->list = l;
@@ -358,11 +440,87 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         }
       }
     }
+  } else if (warp == kSchedWarp) {
+    // ================= item scheduler ==========================================
+    // Pulls work items from the global counter and resolves everything the
+    // producer needs per item (list span, query rows, coarse scores, initial
+    // bounds; L2 prefetch of the rows' A operands) up to kItemSlots items ahead.
+    const int n_items = *P.n_items;
+    uint32_t j = 0;
+    for (;;) {
+      int item = 0;
+      if (lane == 0) item = atomicAdd(P.counter, 1);
+      item = __shfl_sync(kFull, item, 0);
+      const int slot = j % kItemSlots;
+      ItemRec* rec = (ItemRec*)(smem + Lo.items + slot * Lo.item_bytes);
+      if (item >= n_items) {
+        if (j >= (uint32_t)kItemSlots) sm100::mbar_wait(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
+        if (lane == 0) {
+          rec->list = -1;
+          mbar_arrive(&it_full[slot]);
+        }
+        break;
+      }
+      const int2 it = P.items[item];
+      const int l = it.x;
+      const int pbase = P.pstart[l] + it.y * kM;
+      const int nqt = min(kM, P.pstart[l + 1] - pbase);
+      const int size = P.st.list_size[l];
+      const int64_t off = P.st.list_offset[l];
+      const int ntiles = (size + NV - 1) / NV;
+      if (ntiles == 0) {  // empty list: every probing query gets -inf padding
+        for (int r = lane; r < nqt; r += 32) {
+          const int64_t ob = (int64_t)P.pair_idx[pbase + r] * 2 * P.k;
+          for (int p = 0; p < 2 * P.k; ++p) {
+            P.part_s[ob + p] = -INFINITY;
+            P.part_id[ob + p] = INT_MAX;
+          }
+        }
+        continue;
+      }
+      int prow[kM / 32];
+      double pcs[kM / 32];
+      long long kq[kM / 32];
+#pragma unroll
+      for (int q = 0; q < kM / 32; ++q) {
+        const int r = q * 32 + lane;
+        prow[q] = r < nqt ? P.pair_idx[pbase + r] : -1;
+      }
+#pragma unroll
+      for (int q = 0; q < kM / 32; ++q) {
+        pcs[q] = prow[q] >= 0 ? P.coarse[prow[q]] : 0.0;
+        kq[q] = prow[q] >= 0 ? *(volatile const long long*)&P.thr_key[prow[q] / P.n_p] : LLONG_MIN;
+        if (prow[q] >= 0) {  // the decoders read these A rows at the item's first tile
+          const int64_t qo = (int64_t)(prow[q] / P.n_p) * (DP / 2);
+          for (int b = 0; b < DP * 2; b += 128) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(P.q_hi + qo) + b));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"((const char*)(P.q_lo + qo) + b));
+          }
+        }
+      }
+      if (j >= (uint32_t)kItemSlots) sm100::mbar_wait(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
+#pragma unroll
+      for (int q = 0; q < kM / 32; ++q) {
+        rec->prow[q * 32 + lane] = prow[q];
+        rec->cs[q * 32 + lane] = pcs[q];
+        rec->bnd[q * 32 + lane] = prow[q] >= 0 ? prune_bound(kq[q], pcs[q]) : -INFINITY;
+      }
+      if (lane == 0) {
+        rec->list = l;
+        rec->nqt = nqt;
+        rec->size = size;
+        rec->ntiles = ntiles;
+        rec->off = off;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&it_full[slot]);
+      ++j;
+    }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer ===============================================
     const uint32_t idesc = sm100::idesc_f16_f32(kM, NV);
     const uint32_t b_lbo = NV * 16, sbo = 128;
-    const uint32_t qhi_t = tmem + a_col, qlo_t = tmem + a_col + DP / 2;  // A in TMEM
+    uint32_t abuf = 0;  // A buffer of the current item
     uint32_t t = 0, u = 0;
     for (;;) {
       const int ob = t & 1;
@@ -375,30 +533,33 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         break;
       }
       if (c.tile == 0) {
-        sm100::mbar_wait(a_full, u & 1);
+        abuf = u % P.nA;
+        sm100::mbar_wait(&a_full[abuf], (u / P.nA) & 1);
         ++u;
       }
+      const uint32_t qhi_t = tmem + a_col + abuf * DP, qlo_t = qhi_t + DP / 2;  // A in TMEM
       sm100::tc_fence_after();
       TRACE(3);
-      if (lane == 0) {
+      {
+        // whole warp, one elected issuer per instruction; descriptors advance
+        // by a constant (start address field) per K step
         const uint32_t bh = sm100::smem_u32(smem + (ob ? Lo.bhi[1] : Lo.bhi[0]));
         const uint32_t bl = sm100::smem_u32(smem + (ob ? Lo.blo[1] : Lo.blo[0]));
         const uint32_t dt = tmem + ab * NV;
         const int ks = DP / 16;
-        uint32_t acc = 0;
+        const uint64_t dstep = (2 * b_lbo) >> 4;
+        const uint64_t dh = sm100::smem_desc(bh, b_lbo, sbo), dl = sm100::smem_desc(bl, b_lbo, sbo);
+#pragma unroll 1
         for (int pass = 0; pass < 3; ++pass) {
           const uint32_t at = pass == 1 ? qlo_t : qhi_t;
-          const uint32_t ba = pass == 2 ? bl : bh;
-          for (int s = 0; s < ks; ++s) {
-            // K step s: 16 fp16 = 8 TMEM columns of A, two 16-byte chunks of B
-            uint64_t bd = sm100::smem_desc(ba + s * 2 * b_lbo, b_lbo, sbo);
-            sm100::mma_f16_ts(dt, at + s * 8, bd, idesc, acc);
-            acc = 1;
-          }
+          const uint64_t db = pass == 2 ? dl : dh;
+#pragma unroll 4
+          for (int s = 0; s < ks; ++s)
+            sm100::mma_f16_ts_warp(dt, at + s * 8, db + s * dstep, idesc, (pass | s) ? 1u : 0u);
         }
-        sm100::mma_commit(&op_empty[ob]);
-        sm100::mma_commit(&acc_full[ab]);
-        if (c.tile == c.ntiles - 1) sm100::mma_commit(a_empty);
+        sm100::mma_commit_warp(&op_empty[ob]);
+        sm100::mma_commit_warp(&acc_full[ab]);
+        if (c.tile == c.ntiles - 1) sm100::mma_commit_warp(&a_empty[abuf]);
         TRACE(4);
       }
       __syncwarp();
@@ -417,7 +578,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       unsigned char* sp = stage(s);
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       const int ob = t & 1;
+      DTRACE(0);
       if (t >= 2) sm100::mbar_wait(&op_empty[ob], ((t >> 1) - 1) & 1);
+      DTRACE(1);
       if (c.list < 0) {
         // ---- tile record for the MMA issuer and the epilogue (copied out so the
       //      stage slot returns to the producer as soon as decoding is done) ------
@@ -433,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           int* qdst = (int*)(mp + Lo.m_qrow);
           float* nsc = (float*)(mp + Lo.m_nsc);
           int* idd = (int*)(mp + Lo.m_ids);
-          for (int i = dt_; i < kM; i += kDecThreads) qdst[i] = qsrc[i];
+          for (int i = dt_; i < 2 * kM; i += kDecThreads) qdst[i] = qsrc[i];
           for (int v = dt_; v < NV; v += kDecThreads) {
             const bool ok = v < c.valid;
             nsc[v] = ok ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
@@ -453,7 +616,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         // A lives in TMEM: lane = query row, 2 fp16 per 32-bit column along K.
         // Decoder warp w writes TMEM lane quadrant w%4; warps 2..5 the hi
         // halves, 6..9 the lo halves, straight from the pre-split rows.
-        if (u > 0) sm100::mbar_wait(a_empty, (u - 1) & 1);
+        const uint32_t ab_ = u % P.nA;
+        if (u >= (uint32_t)P.nA) sm100::mbar_wait(&a_empty[ab_], ((u / P.nA) - 1) & 1);
+        DTRACE(2);
         sm100::tc_fence_after();
         {
           const int part = (warp - kDecWarp0) >> 2;  // 0 = hi, 1 = lo
@@ -461,25 +626,33 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           const int pi = ((const int*)(sp + Lo.st_qrow))[rrow];
           const uint4* src = (const uint4*)((part ? P.q_lo : P.q_hi) +
                                             (int64_t)(pi >= 0 ? pi / P.n_p : 0) * (DP / 2));
-          const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + a_col + part * (DP / 2);
+          const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + a_col + ab_ * DP +
+                              part * (DP / 2);
+          // four 16-column chunks (a whole DP<=128 row) in flight per round trip
 #pragma unroll 1
-          for (int c16 = 0; c16 < DP / 2; c16 += 16) {
-            uint32_t v[16];
+          for (int c16 = 0; c16 < DP / 2; c16 += 64) {
+            uint32_t v[4][16];
 #pragma unroll
-            for (int x = 0; x < 4; ++x) {
-              const uint4 w4 = pi >= 0 ? __ldg(src + c16 / 4 + x) : make_uint4(0, 0, 0, 0);
-              v[4 * x] = w4.x;
-              v[4 * x + 1] = w4.y;
-              v[4 * x + 2] = w4.z;
-              v[4 * x + 3] = w4.w;
-            }
-            sm100::tmem_st16(ta + c16, v);
+            for (int hh = 0; hh < 4; ++hh)
+#pragma unroll
+              for (int x = 0; x < 4; ++x) {
+                const bool ok = pi >= 0 && c16 + hh * 16 < DP / 2;
+                const uint4 w4 = ok ? __ldg(src + (c16 + hh * 16) / 4 + x) : make_uint4(0, 0, 0, 0);
+                v[hh][4 * x] = w4.x;
+                v[hh][4 * x + 1] = w4.y;
+                v[hh][4 * x + 2] = w4.z;
+                v[hh][4 * x + 3] = w4.w;
+              }
+#pragma unroll
+            for (int hh = 0; hh < 4; ++hh)
+              if (c16 + hh * 16 < DP / 2) sm100::tmem_st16(ta + c16 + hh * 16, v[hh]);
           }
           sm100::tmem_st_wait();
         }
         sm100::tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(a_full);
+        if (lane == 0) mbar_arrive(&a_full[ab_]);
+        DTRACE(3);
         ++u;
       }
       // ---- decode this tile's codes into the B operand ----------------------------
@@ -517,10 +690,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         }
       }
       sm100::fence_proxy_async_smem();
+      DTRACE(4);
       // ---- tile record for the MMA issuer and the epilogue (copied out so the
       //      stage slot returns to the producer as soon as decoding is done) ------
       const int ms = t & (kMeta - 1);
       if (t >= (uint32_t)kMeta) sm100::mbar_wait(&meta_empty[ms], ((t / kMeta) - 1) & 1);
+      DTRACE(5);
       {
         unsigned char* mp = meta(ms);
         if (dt_ == 0) *(Ctrl*)mp = c;
@@ -531,7 +706,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           int* qdst = (int*)(mp + Lo.m_qrow);
           float* nsc = (float*)(mp + Lo.m_nsc);
           int* idd = (int*)(mp + Lo.m_ids);
-          for (int i = dt_; i < kM; i += kDecThreads) qdst[i] = qsrc[i];
+          for (int i = dt_; i < 2 * kM; i += kDecThreads) qdst[i] = qsrc[i];
           for (int v = dt_; v < NV; v += kDecThreads) {
             const bool ok = v < c.valid;
             nsc[v] = ok ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
@@ -552,17 +727,20 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     }
   } else {
     // ================= epilogue =================================================
-    const int et = tid - 32 * kEpiWarp0;   // 0..255
+    // Thread = query row (TMEM lane); the two warps of a lane quadrant split a
+    // tile's columns. Each keeps its own register top-K for the (query, list)
+    // pair and emits it at the item's end as one of the pair's two partial
+    // lists, so the halves never synchronise. Survivors of a 16-column window
+    // (score >= max(own k-th, other half's k-th, global bound)) are taken from
+    // registers one per lane per step; the warp steps max-over-lanes times.
     const int quad = warp & 3;             // TMEM lane quadrant (warp_id % 4)
     const int half = (warp - kEpiWarp0) >> 2;
     const int row = quad * 32 + lane;      // query row == TMEM lane
-    float* cand_v = (float*)(smem + Lo.cand);
-    int* cand_c = (int*)(smem + Lo.cand + cand_entries(KMAX) * kEpiThreads * 4);
-    float* thr_sh = (float*)(smem + Lo.thr);  // [2][kM] running k-th of each half
+    unsigned long long* thr_sh = (unsigned long long*)(smem + Lo.thr);
     RegTopK<KMAX> top;
     top.init();
-    float bnd = -INFINITY;
-    uint32_t t = 0;
+    double cs = 0.0;
+    uint32_t t = 0, tag = 0;
     const int cols = NV / 2;
     for (;;) {
       const int ab = t & (kAcc - 1), ms = t & (kMeta - 1);
@@ -575,8 +753,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       if (P.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarp0 && t < (uint32_t)kTraceTiles)
         P.trace[t * 8 + 7] = c.tile | (c.ntiles << 12) | ((long long)c.nqt << 24);
       const int pi = ((const int*)(mp + Lo.m_qrow))[row];
-      if (c.tile == 0) top.init();
-      if ((c.tile & 3) == 0) bnd = prune_bound(P, pi);
+      const float bnd = ((const float*)(mp + Lo.m_qrow))[kM + row];
+      if (c.tile == 0) {
+        top.init();
+        tag = t + 1;  // identical in both halves: they consume the same tiles
+        cs = pi >= 0 ? P.coarse[pi] : 0.0;  // consumed at the item's end
+      }
       sm100::tc_fence_after();
       const float* nsc = (const float*)(mp + Lo.m_nsc);
       const int* ids = (const int*)(mp + Lo.m_ids);
@@ -586,83 +768,79 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         uint32_t r[32];
         sm100::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
         sm100::tmem_ld_wait();
-        // a candidate must beat this half's k-th, the other half's k-th (either
-        // bounds the pair's top-k) and the query's global bound from other lists
+        ETRACE(0, clock64());
 #pragma unroll
         for (int h = 0; h < 32; h += kDrain) {
-          const float thr = fmaxf(
-              fmaxf(top.s[KMAX - 1], *(volatile float*)&thr_sh[(half ^ 1) * kM + row]), bnd);
-          // survivors of this window go to the thread's own buffer column
-          int cnt = 0;
+          // the other half's k-th bounds this pair too (either half's K
+          // entries are pair candidates); ignore it unless it is this item's
+          const unsigned long long o = *(volatile unsigned long long*)&thr_sh[(half ^ 1) * kM + row];
+          const float oth = (uint32_t)(o >> 32) == tag ? __uint_as_float((uint32_t)o) : -INFINITY;
+          // rows past the item's queries (zero A rows) take nothing
+          const float thr = row < c.nqt ? fmaxf(fmaxf(top.kth(), oth), bnd) : INFINITY;
+          float res[kDrain];
+          uint32_t m = 0;
 #pragma unroll
           for (int e = 0; e < kDrain; e += 4) {
             const float4 f4 = *(const float4*)(nsc + c0 + cc + h + e);
             const float ns[4] = {f4.x, f4.y, f4.z, f4.w};
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
-              const float res = __fmul_rn(__uint_as_float(r[h + e + x]), ns[x]);
-              if (res >= thr) {  // NaN (padding) never passes
-                cand_v[cnt * kEpiThreads + et] = res;
-                cand_c[cnt * kEpiThreads + et] = c0 + cc + h + e + x;
-                ++cnt;
-              }
+              res[e + x] = __fmul_rn(__uint_as_float(r[h + e + x]), ns[x]);
+              m |= (res[e + x] >= thr ? 1u : 0u) << (e + x);  // NaN padding never passes
             }
           }
-          if (__any_sync(kFull, cnt != 0)) {
-            const int mx = __reduce_max_sync(kFull, cnt);
-            for (int i = 0; i < mx; ++i) {
-              if (i < cnt) {
-                const float v = cand_v[i * kEpiThreads + et];
-                const int id = ids[cand_c[i * kEpiThreads + et]];
-                if (top.beats(v, id)) top.insert(v, id);
-              }
-            }
-            *(volatile float*)&thr_sh[half * kM + row] = top.s[KMAX - 1];
+          ETRACE(1 + 3 * (h / kDrain), clock64());
+          if (__any_sync(kFull, m != 0)) {
+            ETRACE(3 + 3 * (h / kDrain), __popc(m));
+            do {
+              const int j = (__ffs(m) - 1) & (kDrain - 1);
+              const float v = pick16(res, j);
+              const int id = ids[c0 + cc + h + j];
+              top.insert(m ? cand_key(v, id) : 0ull);
+              m &= m - 1;
+            } while (__any_sync(kFull, m != 0));
+            *(volatile unsigned long long*)&thr_sh[half * kM + row] =
+                ((unsigned long long)tag << 32) | __float_as_uint(top.kth());
           }
+          ETRACE(2 + 3 * (h / kDrain), clock64());
         }
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[ab]);
-      if (c.tile == c.ntiles - 1) {
-        // merge the column halves of each query row, then emit (query, list) winners
-        if (half == 1) {
+      if (c.tile == c.ntiles - 1 && row < c.nqt) {
+        // this half's partial top-k of the (query, list) pair
+        const int kk = P.k;
+        const int64_t o = ((int64_t)pi * 2 + half) * kk;
+        double sv[KMAX];
+        int iv[KMAX];
 #pragma unroll
-          for (int p = 0; p < KMAX; ++p) {
-            cand_v[p * kEpiThreads + et] = top.s[p];
-            cand_c[p * kEpiThreads + et] = top.i[p];
-          }
+        for (int p = 0; p < KMAX; ++p) {
+          const bool have = top.k[p] != 0;
+          sv[p] = have ? cs + (double)key_score(top.k[p]) : -INFINITY;
+          iv[p] = have ? key_id(top.k[p]) : INT_MAX;
         }
-        named_bar(1, kEpiThreads);
-        if (half == 0 && row < c.nqt) {
-#pragma unroll 1
-          for (int p = 0; p < KMAX; ++p) {
-            const float v = cand_v[p * kEpiThreads + et + 128];
-            const int id = cand_c[p * kEpiThreads + et + 128];
-            if (id != INT_MAX && top.beats(v, id)) top.insert(v, id);
-          }
-          const double cs = P.coarse[pi];
-          const int64_t o = (int64_t)pi * P.k;
+        if (kk == KMAX) {  // 16-byte / 8-byte vector stores (o is even: KMAX is)
 #pragma unroll
-          for (int p = 0; p < KMAX; ++p) {
-            if (p < P.k) {
-              const bool have = top.i[p] != INT_MAX;
-              P.part_s[o + p] = have ? cs + (double)top.s[p] : -INFINITY;
-              P.part_id[o + p] = have ? top.i[p] : INT_MAX;
+          for (int p = 0; p < KMAX; p += 2) {
+            *(double2*)(P.part_s + o + p) = make_double2(sv[p], sv[p + 1]);
+            *(int2*)(P.part_id + o + p) = make_int2(iv[p], iv[p + 1]);
+          }
+        } else {
+#pragma unroll
+          for (int p = 0; p < KMAX; ++p)
+            if (p < kk) {
+              P.part_s[o + p] = sv[p];
+              P.part_id[o + p] = iv[p];
             }
-          }
-          // this pair alone holds KMAX >= k candidates >= its KMAX-th score:
-          // a global lower bound on the query's final k-th, pruning its other
-          // lists (static index keeps the top-K in registers)
-          if (top.i[KMAX - 1] != INT_MAX)
-            atomicMax(&P.thr_key[pi / P.n_p], dkey(cs + (double)top.s[KMAX - 1]));
         }
-        // reset the shared half thresholds for the next item before anyone
-        // can read them again (next read follows this barrier)
-        thr_sh[half * kM + row] = -INFINITY;
-        named_bar(1, kEpiThreads);
+        // KMAX >= k candidates of this query score >= this K-th: a global lower
+        // bound on its final k-th that prunes its other lists
+        if (top.k[KMAX - 1] != 0)
+          atomicMax(&P.thr_key[pi / P.n_p], dkey(cs + (double)key_score(top.k[KMAX - 1])));
       }
       __syncwarp();
+      ETRACE(7, clock64());
       if (warp == kEpiWarp0) TRACE(6);
       if (lane == 0) mbar_arrive(&meta_empty[ms]);
       ++t;
@@ -871,8 +1049,8 @@ static TcScratch carve_tc(void* base, int64_t nq, int n_p, int L, int k, int dim
   S.q_hi = (uint32_t*)take(4 * (size_t)nq * (pad_dp(dim) / 2));
   S.q_lo = (uint32_t*)take(4 * (size_t)nq * (pad_dp(dim) / 2));
   S.items = (int2*)take(8 * (size_t)max_items);
-  S.part_s = (double*)take(8 * (size_t)np * k);
-  S.part_id = (int32_t*)take(4 * (size_t)np * k);
+  S.part_s = (double*)take(8 * (size_t)np * 2 * k);  // two partial lists per pair
+  S.part_id = (int32_t*)take(4 * (size_t)np * 2 * k);
   S.bytes = off;
   return S;
 }
@@ -984,14 +1162,15 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   const char* trace_path = getenv("IVFTQ_TRACE");
   long long* trace = nullptr;
   if (trace_path) {
-    cudaMalloc(&trace, sizeof(long long) * 8 * kTraceTiles);
-    cudaMemsetAsync(trace, 0, sizeof(long long) * 8 * kTraceTiles, s);
+    cudaMalloc(&trace, sizeof(long long) * 24 * kTraceTiles);
+    cudaMemsetAsync(trace, 0, sizeof(long long) * 24 * kTraceTiles, s);
   }
   P.trace = trace;
   P.n_p = n_p;
   P.k = depth;
   P.d = st->dim;
   P.DP = DP;
+  P.nA = (kAcc * kNV + 2 * DP <= 512) ? 2 : 1;
   // Every Lloyd-Max level satisfies |T| < 5/sqrt(d) < 4, so 2^12 keeps the
   // scaled table below 2^14 and its hi/lo halves in the fp16 normal range.
   const int eT = 12;
@@ -1012,7 +1191,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
 #undef TC_CASE
   if (rc) return rc;
   if (trace) {
-    static long long h[8 * kTraceTiles];
+    static long long h[24 * kTraceTiles];
     cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
     cudaStreamSynchronize(s);
     FILE* f = fopen(trace_path, "w");
@@ -1027,9 +1206,36 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
       }
       fclose(f);
     }
+    std::string dp = std::string(trace_path) + ".dec";
+    f = fopen(dp.c_str(), "w");
+    if (f) {
+      fprintf(f, "# t after_stfull after_opempty after_aempty after_abuild after_decode after_metaempty (rel. dec_start)\n");
+      for (int t = 0; t < kTraceTiles; ++t) {
+        const long long* e = h + 16 * kTraceTiles + t * 8;
+        if (!h[t * 8 + 1]) break;
+        const long long b = h[t * 8 + 1];
+        fprintf(f, "%d", t);
+        for (int k = 0; k < 6; ++k) fprintf(f, " %lld", e[k] ? e[k] - b : -1);
+        fprintf(f, "\n");
+      }
+      fclose(f);
+    }
+    std::string ep = std::string(trace_path) + ".epi";
+    f = fopen(ep.c_str(), "w");
+    if (f) {
+      fprintf(f, "# t ld_done w0_filter w0_drain w0_mx w1_filter w1_drain w1_mx end (rel. epi_start)\n");
+      for (int t = 0; t < kTraceTiles; ++t) {
+        const long long* e = h + 8 * kTraceTiles + t * 8;
+        if (!h[t * 8 + 1]) break;
+        const long long b = h[t * 8 + 5];
+        fprintf(f, "%d %lld %lld %lld %lld %lld %lld %lld %lld\n", t, e[0] - b, e[1] - b,
+                e[2] - b, e[3], e[4] - b, e[5] - b, e[6], e[7] - b);
+      }
+      fclose(f);
+    }
     cudaFree(trace);
   }
   if (int e = merge_smem_opt_in(depth)) return e;
-  launch_merge(S.part_s, S.part_id, nq, n_p * depth, depth, ids_out, scores_out, s);
+  launch_merge(S.part_s, S.part_id, nq, n_p * 2 * depth, depth, ids_out, scores_out, s);
   return check_launch("merge");
 }

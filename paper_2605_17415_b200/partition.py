@@ -85,39 +85,6 @@ class _HostOps:
         return a @ v
 
 
-class _DeviceOps:
-    """f64 products on the GPU through ivftq_gemm_nt (same math, other order)."""
-
-    def __init__(self, data: np.ndarray):
-        import torch
-
-        from . import _lib
-
-        self.torch = torch
-        self.L = _lib.lib()
-        self._lib = _lib
-        self.dev = torch.device("cuda", torch.cuda.current_device())
-        self.data_h = data
-        self.data = torch.from_numpy(np.ascontiguousarray(data)).to(self.dev)
-
-    def ip(self, a, b):
-        t = self.torch
-        if a is self.data_h:
-            A = self.data
-        else:
-            A = t.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(self.dev)
-        B = t.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(self.dev)
-        out = t.empty((A.shape[0], B.shape[0]), dtype=t.float64, device=self.dev)
-        self._lib.check(self.L.ivftq_gemm_nt(A.data_ptr(), B.data_ptr(), self._lib.IVFTQ_F64,
-                                             A.shape[0], B.shape[0], A.shape[1],
-                                             out.data_ptr(), self._lib.IVFTQ_F64,
-                                             self._lib.stream_ptr()), "gemm_nt")
-        return out.cpu().numpy()
-
-    def ipv(self, a, v):
-        return self.ip(a, v[None, :])[:, 0]
-
-
 def _kmeanspp(data, k, rng, ops):
     n = data.shape[0]
     nc = 2 + int(np.log2(k)) if k > 1 else 1
@@ -158,7 +125,9 @@ def train_partition(data: np.ndarray, n_lists: int, seed: int, max_iters: int = 
         raise ValueError(f"need at least n_lists={n_lists} rows, got {n}")
     if np.any(np.linalg.norm(data, axis=1) < _EPS):
         raise ValueError("zero-norm row in training data")
-    ops = _DeviceOps(data) if device == "cuda" else _HostOps()
+    if device == "cuda":
+        return _train_device(data, n_lists, seed, max_iters)
+    ops = _HostOps()
     rng = np.random.default_rng(seed)
     cent = _kmeanspp(data, n_lists, rng, ops)
     prev = None
@@ -192,4 +161,99 @@ def train_partition(data: np.ndarray, n_lists: int, seed: int, max_iters: int = 
     counts = np.bincount(final, minlength=n_lists)
     lists = [m.tolist() for m in np.split(order, np.cumsum(counts)[:-1])]
     return CoarsePartition(n_lists=n_lists, dim=dim, centroids=cent.astype(np.float32),
+                           lists=lists)
+
+
+def _train_device(data: np.ndarray, n_lists: int, seed: int, max_iters: int,
+                  chunk: int = 1 << 16) -> CoarsePartition:
+    """The same algorithm and RNG call sequence as the host path, with the data
+    resident on the GPU: f64 products through ivftq_gemm_nt, the n-long
+    k-means++ potential and Lloyd sums kept on the device (sums by a
+    deterministic segmented reduction over rows sorted by list). Only the
+    sampling vector p (8n bytes per seeding step) and a few scalars cross to
+    the host. Results differ from the host path only through f64 summation
+    order; memory is O(n*d + chunk*L), so it trains 1M x 4096 in one pass.
+    """
+    import torch
+
+    from . import _lib
+
+    L = _lib.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    f64 = torch.float64
+    X = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dev)
+    n, dim = X.shape
+    k = n_lists
+    rng = np.random.default_rng(seed)
+
+    def gemm(A, B):
+        out = torch.empty((A.shape[0], B.shape[0]), dtype=f64, device=dev)
+        _lib.check(L.ivftq_gemm_nt(A.data_ptr(), B.data_ptr(), _lib.IVFTQ_F64, A.shape[0],
+                                   B.shape[0], dim, out.data_ptr(), _lib.IVFTQ_F64,
+                                   _lib.stream_ptr()), "gemm_nt")
+        return out
+
+    def argmax_ip(C):
+        a = torch.empty(n, dtype=torch.int64, device=dev)
+        best = torch.empty(n, dtype=f64, device=dev)
+        for s0 in range(0, n, chunk):
+            v, i = gemm(X[s0:s0 + chunk], C).max(dim=1)  # first maximal index on ties
+            a[s0:s0 + chunk] = i
+            best[s0:s0 + chunk] = v
+        return a, best
+
+    def dist2(rows):
+        return torch.clamp(2.0 - 2.0 * gemm(X, X[torch.as_tensor(rows, device=dev)]), min=0.0)
+
+    # ---- k-means++ seeding (partition.py:_kmeanspp) ----
+    nc = 2 + int(np.log2(k)) if k > 1 else 1
+    chosen = np.empty(k, dtype=np.int64)
+    chosen[0] = rng.integers(n)
+    d2 = dist2([chosen[0]])[:, 0].contiguous()
+    for j in range(1, k):
+        tot = float(d2.sum().item())
+        if tot <= _EPS:
+            keep = np.ones(n, dtype=bool)
+            keep[chosen[:j]] = False
+            pool = np.flatnonzero(keep)
+            chosen[j] = rng.choice(pool) if len(pool) else rng.integers(n)
+            d2 = torch.minimum(d2, dist2([chosen[j]])[:, 0])
+            continue
+        p = (d2 / tot).cpu().numpy()
+        cand = rng.choice(n, size=nc, p=p / p.sum())
+        cd2 = dist2(cand)
+        pot = torch.minimum(d2[:, None], cd2).sum(dim=0).cpu().numpy()
+        b = int(np.argmin(pot))
+        chosen[j] = cand[b]
+        d2 = torch.minimum(d2, cd2[:, b]).contiguous()
+    cent = X[torch.as_tensor(chosen, device=dev)].clone()
+
+    # ---- Lloyd iterations (partition.py:147-170) ----
+    prev = None
+    for _ in range(max_iters):
+        a, best = argmax_ip(cent)
+        if prev is not None and torch.equal(a, prev):
+            break
+        prev = a
+        cnt = torch.bincount(a, minlength=k)
+        order = torch.argsort(a, stable=True)
+        sums = torch.segment_reduce(X[order], "sum", lengths=cnt, axis=0)
+        cnt_h = cnt.cpu().numpy()
+        empty = np.flatnonzero(cnt_h == 0)
+        if len(empty):
+            far = torch.argsort(best, stable=True)[: len(empty)]
+            sums[torch.as_tensor(empty, device=dev)] = X[far]
+        nn = torch.linalg.vector_norm(sums, dim=1)
+        bad = np.flatnonzero((nn < _EPS).cpu().numpy())
+        if len(bad):
+            for slot in bad:
+                sums[int(slot)] = X[int(rng.integers(n))]
+            nn = torch.linalg.vector_norm(sums, dim=1)
+        cent = sums / nn[:, None]
+    final, _ = argmax_ip(cent)
+    final = final.cpu().numpy()
+    order = np.argsort(final, kind="stable")
+    counts = np.bincount(final, minlength=k)
+    lists = [m.tolist() for m in np.split(order, np.cumsum(counts)[:-1])]
+    return CoarsePartition(n_lists=k, dim=dim, centroids=cent.cpu().numpy().astype(np.float32),
                            lists=lists)

@@ -60,6 +60,148 @@ __global__ void bench(int iters, unsigned long long* out) {
   if (tid < 32) sm100::tmem_dealloc(tmem, 256);
 }
 
+// A operand from TMEM (.ts form): columns [256, 256 + 64) hold A (K = 128 as
+// 8 K-steps x 8 columns), accumulator at column 0 (N <= 256).
+template <int N>
+__global__ void bench_ts(int iters, unsigned long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N * 128; i += blockDim.x) ((uint16_t*)smem)[i] = 0x3c00;
+  if (tid < 32) sm100::tmem_alloc(&tslot, 512);
+  if (tid == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::mbar_fence_init();
+  }
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t b = sm100::smem_u32(smem);
+  const uint32_t idesc = sm100::idesc_f16_f32(128, N);
+  if (tid == 0) {
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      for (int s = 0; s < 8; ++s) {
+        uint64_t bd = sm100::smem_desc(b + s * 2 * N * 16, N * 16, 128);
+        sm100::mma_f16_ts(tmem, tmem + 256 + s * 8, bd, idesc, (it | s) ? 1u : 0u);
+      }
+    }
+    sm100::mma_commit(&bar);
+    sm100::mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) sm100::tmem_dealloc(tmem, 512);
+}
+
+// Same MMA stream while other warps load the machine: mode 1 = 8 warps
+// streaming 16-byte shared-memory stores + loads, mode 2 = 4 warps reading
+// TMEM (tcgen05.ld 32 columns) in a loop, mode 3 = both.
+template <int N>
+__global__ void bench_ts_busy(int iters, int mode, unsigned long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ uint32_t tslot;
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ volatile int done;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < N * 128; i += blockDim.x) ((uint16_t*)smem)[i] = 0x3c00;
+  if (tid < 32) sm100::tmem_alloc(&tslot, 512);
+  if (tid == 0) {
+    sm100::mbar_init(&bar, 1);
+    sm100::mbar_fence_init();
+    done = 0;
+  }
+  sm100::fence_proxy_async_smem();
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tslot;
+  const uint32_t b = sm100::smem_u32(smem);
+  const uint32_t idesc = sm100::idesc_f16_f32(128, N);
+  unsigned char* scratch = smem + N * 128 * 2;
+  if (warp == 0) {
+    if (tid == 0) {
+      long long t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        for (int s = 0; s < 8; ++s) {
+          uint64_t bd = sm100::smem_desc(b + s * 2 * N * 16, N * 16, 128);
+          sm100::mma_f16_ts(tmem, tmem + 256 + s * 8, bd, idesc, (it | s) ? 1u : 0u);
+        }
+      }
+      sm100::mma_commit(&bar);
+      sm100::mbar_wait(&bar, 0);
+      long long t1 = clock64();
+      out[blockIdx.x] = (unsigned long long)(t1 - t0);
+      done = 1;
+    }
+  } else if (warp >= 1 && warp <= 8) {
+    if (mode & 1) {
+      uint4* p = (uint4*)scratch + (warp - 1) * 32 * 16 + (tid & 31);
+      uint4 v = make_uint4(tid, 1, 2, 3);
+      while (!done) {
+        for (int i = 0; i < 16; ++i) {
+          p[i * 32] = v;
+          v.x += ((volatile uint4*)p)[((i + 5) & 15) * 32].y;
+        }
+      }
+      if (v.x == 12345) out[148 + tid] = v.x;
+    }
+  } else if (warp >= 9 && warp <= 12) {
+    if (mode & 2) {
+      uint32_t acc = 0;
+      const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + 384;
+      while (!done) {
+        uint32_t r[32];
+        sm100::tmem_ld32(ta, r);
+        sm100::tmem_ld_wait();
+        acc += r[0] + r[31];
+      }
+      if (acc == 12345) out[148 + tid] = acc;
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (tid < 32) sm100::tmem_dealloc(tmem, 512);
+}
+
+template <int N>
+void run_ts_busy(int mode) {
+  unsigned long long* d;
+  cudaMalloc(&d, (148 + 1024) * 8);
+  int iters = 2000;
+  size_t smem = N * 128 * 2 + 8 * 32 * 16 * 16 + 1024;
+  cudaFuncSetAttribute(bench_ts_busy<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bench_ts_busy<N><<<148, 13 * 32, smem>>>(iters, mode, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double cyc = (double)h[0] / (iters * 8);
+  printf("ts busy mode %d N=%3d: %7.1f cycles/MMA  (%s)\n", mode, N, cyc, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
+template <int N>
+void run_ts() {
+  unsigned long long* d;
+  cudaMalloc(&d, 148 * 8);
+  int iters = 2000;
+  size_t smem = N * 128 * 2 + 1024;
+  cudaFuncSetAttribute(bench_ts<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  bench_ts<N><<<148, 128, smem>>>(iters, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double cyc = (double)h[0] / (iters * 8);
+  printf("%-14s N=%3d: %7.1f cycles/MMA  %7.0f flop/cyc/SM  (%s)\n", "ts(A in TMEM)", N, cyc,
+         2.0 * 128 * N * 16 / cyc, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 template <int N, bool SW>
 void run(const char* name) {
   unsigned long long* d;
@@ -85,5 +227,10 @@ int main() {
   run<64, true>("swizzle128");
   run<128, true>("swizzle128");
   run<256, true>("swizzle128");
+  run_ts<64>();
+  run_ts<128>();
+  run_ts<256>();
+  for (int m = 0; m < 4; ++m) run_ts_busy<64>(m);
+  for (int m = 0; m < 4; ++m) run_ts_busy<128>(m);
   return 0;
 }

@@ -415,3 +415,18 @@ class TestRefresh:
         rec = reconstruct_all(idx)
         np.testing.assert_allclose(rec, orc.reconstruct_all(o), rtol=0, atol=1e-13)
         np.testing.assert_allclose(reconstruct_vector(idx, 123), rec[123], atol=1e-15)
+
+
+@pytest.mark.parametrize("name", ["d32_b4_L16_raw", "d128_b4_L64", "d200_b3_L16"])
+def test_train_partition_device_matches_reference(golden, name):
+    """GPU k-means (same algorithm and RNG sequence, f64 products on the device)
+    against the reference's centroids: identical up to f64 summation order."""
+    from paper_2605_17415_b200.partition import train_partition
+
+    g = golden(name)
+    x = g["x"].astype(np.float64)
+    xn = x / np.linalg.norm(x, axis=1)[:, None]
+    p = train_partition(xn, int(g["config"][2]), seed=int(g["config"][7]), device="cuda")
+    np.testing.assert_allclose(p.centroids, g["centroids"], rtol=0, atol=1e-6)
+    sizes = np.array([len(m) for m in p.lists])
+    assert sizes.sum() == len(x)
