@@ -69,28 +69,6 @@ constexpr int kNV = 64;          // vectors per tile (MMA N)
 // TMEM budget: kAcc accumulators of kNV columns + the A operand (DP columns)
 constexpr int kMaxDim = 512 - kAcc * kNV;
 
-struct Params {
-  ivftq_store st;
-  const double* coarse;    // [nq*n_p] coarse score of pair (q, p)
-  const float* qrot;       // [nq*d]
-  const double* levels;    // [2^(bits+1)]
-  const int32_t* pair_idx; // pair flat index q*n_p+p, grouped by list
-  const int32_t* pstart;   // [L+1] first grouped pair of each list
-  const int2* items;       // (list, query tile)
-  const int32_t* n_items;  // device scalar
-  int32_t* counter;        // work counter (zeroed per launch)
-  double* part_s;          // [nq*n_p*k]
-  int32_t* part_id;
-  long long* thr_key;      // [nq] order-preserving key of a lower bound on the k-th score
-  long long* trace;        // debug timeline of CTA 0 (IVFTQ_TRACE), else null
-  const uint32_t* q_hi;    // [nq][DP/2] rotated query rows, fp16 hi halves (x 2^14), packed pairs
-  const uint32_t* q_lo;    // [nq][DP/2] matching lo halves
-  int n_p, k, d, DP, NV, NS;
-  int nA;           // A-operand buffers in TMEM (2 when they fit: next item's
-                    // queries are written while the current item's MMAs run)
-  float t_scale;    // 2^eT
-  float inv_scale;  // 2^-(eT+14)
-};
 
 // control record of one tile in a stage slot
 struct Ctrl {
@@ -162,6 +140,30 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.total = off;
   return L;
 }
+
+struct Params {
+  ivftq_store st;
+  const double* coarse;    // [nq*n_p] coarse score of pair (q, p)
+  const float* qrot;       // [nq*d]
+  const double* levels;    // [2^(bits+1)]
+  const int32_t* pair_idx; // pair flat index q*n_p+p, grouped by list
+  const int32_t* pstart;   // [L+1] first grouped pair of each list
+  const int2* items;       // (list, query tile)
+  const int32_t* n_items;  // device scalar
+  int32_t* counter;        // work counter (zeroed per launch)
+  double* part_s;          // [nq*n_p*k]
+  int32_t* part_id;
+  long long* thr_key;      // [nq] order-preserving key of a lower bound on the k-th score
+  long long* trace;        // debug timeline of CTA 0 (IVFTQ_TRACE), else null
+  const uint32_t* q_hi;    // [nq][DP/2] rotated query rows, fp16 hi halves (x 2^14), packed pairs
+  const uint32_t* q_lo;    // [nq][DP/2] matching lo halves
+  int n_p, k, d, DP, NV, NS;
+  int nA;           // A-operand buffers in TMEM (2 when they fit: next item's
+                    // queries are written while the current item's MMAs run)
+  float t_scale;    // 2^eT
+  float inv_scale;  // 2^-(eT+14)
+  Layout lo;        // shared-memory carve-up, computed once on the host
+};
 
 __device__ __forceinline__ uint32_t split_pack(float x, uint32_t& lo) {
   __half h = __float2half_rn(x);
@@ -301,8 +303,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   const uint32_t a_col = kAcc * NV;
   const uint32_t need = a_col + P.nA * DP;
   const uint32_t tmem_cols = need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
-  const Layout Lo = make_layout(NV, NS, DP, W, C, KMAX);
-  uint32_t* tab = (uint32_t*)(smem + Lo.tab);
+  const Layout& Lo = P.lo;  // kernel-parameter space: no per-use recomputation
+  // level table in static shared memory: lookups address it as reg + symbol
+  __shared__ uint32_t s_tab[C];
+  uint32_t* tab = s_tab;
   uint64_t* bars = (uint64_t*)(smem + Lo.bars);
   uint64_t* st_full = bars;            // [NS] producer -> decoders/epilogue (TMA tx)
   uint64_t* st_empty = bars + 8;       // [NS] decoders + epilogue -> producer
@@ -370,12 +374,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0, j = 0;
     for (;;) {
       const int slot = j % kItemSlots;
-      sm100::mbar_wait(&it_full[slot], (j / kItemSlots) & 1);
+      sm100::mbar_wait_sleep(&it_full[slot], (j / kItemSlots) & 1);
       const ItemRec* rec = (const ItemRec*)(smem + Lo.items + slot * Lo.item_bytes);
       const int l = rec->list;
       if (l < 0) {
         const int s = t % NS;
-        if (t >= (uint32_t)NS) sm100::mbar_wait(&st_empty[s], ((t / NS) - 1) & 1);
+        if (t >= (uint32_t)NS) sm100::mbar_wait_sleep(&st_empty[s], ((t / NS) - 1) & 1);
         if (lane == 0) {
           Ctrl* c = (Ctrl*)(stage(s) + Lo.st_ctrl);
           c->list = -1;
@@ -411,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
                                  : LLONG_MIN;
         }
         const int s = t % NS;
-        if (t >= (uint32_t)NS) sm100::mbar_wait(&st_empty[s], ((t / NS) - 1) & 1);
+        if (t >= (uint32_t)NS) sm100::mbar_wait_sleep(&st_empty[s], ((t / NS) - 1) & 1);
         unsigned char* sp = stage(s);
         int* qrow = (int*)(sp + Lo.st_qrow);
         float* qb = (float*)(qrow + kM);
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const int slot = j % kItemSlots;
       ItemRec* rec = (ItemRec*)(smem + Lo.items + slot * Lo.item_bytes);
       if (item >= n_items) {
-        if (j >= (uint32_t)kItemSlots) sm100::mbar_wait(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
+        if (j >= (uint32_t)kItemSlots) sm100::mbar_wait_sleep(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
         if (lane == 0) {
           rec->list = -1;
           mbar_arrive(&it_full[slot]);
@@ -498,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           }
         }
       }
-      if (j >= (uint32_t)kItemSlots) sm100::mbar_wait(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
+      if (j >= (uint32_t)kItemSlots) sm100::mbar_wait_sleep(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
 #pragma unroll
       for (int q = 0; q < kM / 32; ++q) {
         rec->prow[q * 32 + lane] = prow[q];
@@ -573,19 +577,19 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0, u = 0;
     for (;;) {
       const int s = t % NS;
-      sm100::mbar_wait(&st_full[s], (t / NS) & 1);
+      sm100::mbar_wait_sleep(&st_full[s], (t / NS) & 1);
       if (warp == kDecWarp0) TRACE(1);
       unsigned char* sp = stage(s);
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       const int ob = t & 1;
       DTRACE(0);
-      if (t >= 2) sm100::mbar_wait(&op_empty[ob], ((t >> 1) - 1) & 1);
+      if (t >= 2) sm100::mbar_wait_sleep(&op_empty[ob], ((t >> 1) - 1) & 1);
       DTRACE(1);
       if (c.list < 0) {
         // ---- tile record for the MMA issuer and the epilogue (copied out so the
       //      stage slot returns to the producer as soon as decoding is done) ------
       const int ms = t & (kMeta - 1);
-      if (t >= (uint32_t)kMeta) sm100::mbar_wait(&meta_empty[ms], ((t / kMeta) - 1) & 1);
+      if (t >= (uint32_t)kMeta) sm100::mbar_wait_sleep(&meta_empty[ms], ((t / kMeta) - 1) & 1);
       {
         unsigned char* mp = meta(ms);
         if (dt_ == 0) *(Ctrl*)mp = c;
@@ -617,7 +621,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         // Decoder warp w writes TMEM lane quadrant w%4; warps 2..5 the hi
         // halves, 6..9 the lo halves, straight from the pre-split rows.
         const uint32_t ab_ = u % P.nA;
-        if (u >= (uint32_t)P.nA) sm100::mbar_wait(&a_empty[ab_], ((u / P.nA) - 1) & 1);
+        if (u >= (uint32_t)P.nA) sm100::mbar_wait_sleep(&a_empty[ab_], ((u / P.nA) - 1) & 1);
         DTRACE(2);
         sm100::tc_fence_after();
         {
@@ -673,19 +677,22 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         for (int cc = 0; cc < GC; ++cc) {
           const int ch = gi * GC + cc;
           if (ch < NCH) {
-            uint32_t hi[8], lo[8];
+            uint32_t tv[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int f = cc * 8 + e;  // field within group (compile time)
-              const uint32_t tv = tab[(words[f / FPW] >> ((f % FPW) * FB)) & MASK];
-              hi[e] = tv & 0xFFFFu;
-              lo[e] = tv >> 16;
+              tv[e] = s_tab[(words[f / FPW] >> ((f % FPW) * FB)) & MASK];
             }
+            // entry = hi | lo << 16: one byte permute packs each fp16 pair
             const uint32_t o = ch * (NV * 16) + (v >> 3) * 128 + (v & 7) * 16;
-            *(uint4*)(bhi + o) = make_uint4(hi[0] | (hi[1] << 16), hi[2] | (hi[3] << 16),
-                                            hi[4] | (hi[5] << 16), hi[6] | (hi[7] << 16));
-            *(uint4*)(blo + o) = make_uint4(lo[0] | (lo[1] << 16), lo[2] | (lo[3] << 16),
-                                            lo[4] | (lo[5] << 16), lo[6] | (lo[7] << 16));
+            *(uint4*)(bhi + o) = make_uint4(__byte_perm(tv[0], tv[1], 0x5410),
+                                            __byte_perm(tv[2], tv[3], 0x5410),
+                                            __byte_perm(tv[4], tv[5], 0x5410),
+                                            __byte_perm(tv[6], tv[7], 0x5410));
+            *(uint4*)(blo + o) = make_uint4(__byte_perm(tv[0], tv[1], 0x7632),
+                                            __byte_perm(tv[2], tv[3], 0x7632),
+                                            __byte_perm(tv[4], tv[5], 0x7632),
+                                            __byte_perm(tv[6], tv[7], 0x7632));
           }
         }
       }
@@ -694,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       // ---- tile record for the MMA issuer and the epilogue (copied out so the
       //      stage slot returns to the producer as soon as decoding is done) ------
       const int ms = t & (kMeta - 1);
-      if (t >= (uint32_t)kMeta) sm100::mbar_wait(&meta_empty[ms], ((t / kMeta) - 1) & 1);
+      if (t >= (uint32_t)kMeta) sm100::mbar_wait_sleep(&meta_empty[ms], ((t / kMeta) - 1) & 1);
       DTRACE(5);
       {
         unsigned char* mp = meta(ms);
@@ -744,8 +751,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     const int cols = NV / 2;
     for (;;) {
       const int ab = t & (kAcc - 1), ms = t & (kMeta - 1);
-      sm100::mbar_wait(&acc_full[ab], (t / kAcc) & 1);
-      sm100::mbar_wait(&meta_full[ms], (t / kMeta) & 1);
+      sm100::mbar_wait_sleep(&acc_full[ab], (t / kAcc) & 1);
+      sm100::mbar_wait_sleep(&meta_full[ms], (t / kMeta) & 1);
       const unsigned char* mp = meta(ms);
       const Ctrl c = *(const Ctrl*)mp;
       if (c.list < 0) break;
@@ -1176,7 +1183,8 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   const int eT = 12;
   P.t_scale = ldexpf(1.0f, eT);
   P.inv_scale = ldexpf(1.0f, -(eT + 14));
-  size_t smem = make_layout(P.NV, P.NS, DP, st->words_per_vec, C, kmax).total + 1024;
+  P.lo = make_layout(P.NV, P.NS, DP, st->words_per_vec, C, kmax);
+  size_t smem = P.lo.total + 1024;
   int grid = g_num_sms;
   int rc;
 #define TC_CASE(FBV)                                                              \

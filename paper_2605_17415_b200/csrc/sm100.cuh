@@ -42,6 +42,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Same for warps off the critical path: between polls the warp sleeps ~64 ns,
+// so idle roles stop taking issue slots from the busy warps of their SM
+// sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAITS:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
+      "@P1 bra DONES;\n"
+      "nanosleep.u32 64;\n"
+      "bra LAB_WAITS;\n"
+      "DONES:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
+
 // ---- 1-D TMA bulk copy global -> shared, completion on an mbarrier -----------
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
