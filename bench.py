@@ -341,7 +341,7 @@ def run_ours(args):
     qnd, bad, _ = idx._normalize_queries_device(Qd)
     probe = torch.empty((nq, n_p), dtype=torch.int32, device=dev)
     coarse = torch.empty((nq, n_p), dtype=torch.float64, device=dev)
-    pb = L.ivftq_probe_scratch_bytes(nq, w.n_lists)
+    pb = L.ivftq_probe_scratch_bytes(nq, w.n_lists, w.d)
     pscr = torch.empty(pb, dtype=torch.uint8, device=dev)
     s = _lib.stream_ptr()
     _lib.check(L.ivftq_probe(qnd.data_ptr(), idx._cent.data_ptr(), nq, w.n_lists, w.d, n_p,

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define IVFTQ_ABI_VERSION 1
+#define IVFTQ_ABI_VERSION 2
 
 #define IVFTQ_OK 0
 #define IVFTQ_ERR_ARG (-1)
@@ -87,9 +87,28 @@ int ivftq_normalize_rows(const void* x, int x_dtype, int64_t n, int dim,
  * f64/f32: coarse scores (index.py:436), rotations (rotation.py:40). */
 int ivftq_gemm_nt(const double* A, const void* B, int b_dtype, int64_t M, int N,
                   int K, void* C, int c_dtype, void* stream);
-/* Max-IP list per row, ties -> lowest list (partition.py:45-55). */
+/* Max-IP list per row, ties -> lowest list (partition.py:45-55), f64 DFMA. */
 int ivftq_assign(const double* xn, const float* centroids, int64_t n, int n_lists,
                  int dim, int32_t* list_out, void* stream);
+/* Same decision on the tensor cores: error-compensated fp16 tcgen05 GEMM keeps
+ * each row's best four approximate scores, then every centroid within the
+ * error band of the maximum is re-scored in exact f64 (identical values and
+ * tie rule to ivftq_assign). Falls back to ivftq_assign when unsupported. */
+size_t ivftq_assign_tc_scratch_bytes(int64_t n, int n_lists, int dim);
+int ivftq_assign_tc(const double* xn, const float* centroids, int64_t n, int n_lists,
+                    int dim, int32_t* list_out, void* scratch, size_t scratch_bytes,
+                    void* stream);
+/* Coarse-scoring path selection (results are identical in every mode):
+ * 0 = default: assignment on tensor cores with the f64 guard band (dim <= 256),
+ *     probes on the f64 GEMM + exact select;
+ * 1 = f64 CUDA-core GEMMs only (parity reference);
+ * 2 = tensor cores for probes as well (also IVFTQ_PROBE_TC=1). */
+int ivftq_set_coarse_mode(int mode);
+int ivftq_coarse_tc_supported(int dim, int n_lists);
+/* Pre-split centroid operand images for the tensor-core coarse GEMM. */
+size_t ivftq_coarse_prep_bytes(int n_lists, int dim);
+int ivftq_coarse_prepare(const float* centroids, int n_lists, int dim, void* prep,
+                         void* stream);
 /* Residual r = xn - c_l (or xn when flat), ||r|| -> binary16 (index.py:247-255). */
 int ivftq_residuals(const double* xn, const float* centroids, const int32_t* list_ids,
                     int64_t n, int dim, int flat, double* resid_out,
@@ -101,9 +120,9 @@ int ivftq_quantize_pack(const double* rot, const uint16_t* norms, int64_t n, int
                         int bits, int use_sign, const double* boundaries,
                         const double* qcent, uint32_t* words_out, void* stream);
 /* Whole encoder: normalize -> assign -> residual -> rotate -> quantize/pack.
- * scratch >= ivftq_encode_scratch_bytes(n, dim). Outputs per row: xn (f64, for
+ * scratch >= ivftq_encode_scratch_bytes(n, dim, n_lists). Outputs per row: xn (f64, for
  * the raw store; may alias nothing), list id, binary16 norm, code words. */
-size_t ivftq_encode_scratch_bytes(int64_t n, int dim);
+size_t ivftq_encode_scratch_bytes(int64_t n, int dim, int n_lists);
 int ivftq_encode(const void* x, int x_dtype, int64_t n, int dim, int bits, int use_sign,
                  int flat, const float* centroids, int n_lists, const double* R,
                  const double* boundaries, const double* qcent, double* xn_out,
@@ -141,8 +160,10 @@ int ivftq_xor_codes(const ivftq_store* store, const int64_t* slot_of, int64_t n,
  * -> idx_out/val_out (rows, n), the stable argsort probe order (index.py:438). */
 int ivftq_select_topn(const double* scores, int64_t rows, int cols, int n,
                       int32_t* idx_out, double* val_out, void* stream);
-/* Coarse probes: scores qn.C^T in f64 then select (index.py:436-438). */
-size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists);
+/* Coarse probes (index.py:436-438): stable top-n_p of qn.C^T. Tensor-core
+ * scores + exact f64 re-scoring of the guard band when supported, else the
+ * f64 GEMM + select; both return identical probes and f64 coarse values. */
+size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists, int dim);
 int ivftq_probe(const double* qn, const float* centroids, int64_t nq, int n_lists,
                 int dim, int n_p, int32_t* probe_out, double* coarse_out,
                 void* scratch, size_t scratch_bytes, void* stream);

@@ -58,7 +58,7 @@ _SIGS = {
     "ivftq_assign": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
     "ivftq_residuals": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "ivftq_quantize_pack": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
-    "ivftq_encode_scratch_bytes": (_sz, [_i64, _i32]),
+    "ivftq_encode_scratch_bytes": (_sz, [_i64, _i32, _i32]),
     "ivftq_encode": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp,
                             _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ivftq_pack_codes": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),
@@ -68,7 +68,13 @@ _SIGS = {
     "ivftq_export_codes": (_i32, [C.POINTER(IvftqStore), _vp, _i64, _i64, _vp, _vp, _vp]),
     "ivftq_xor_codes": (_i32, [C.POINTER(IvftqStore), _vp, _i64, _vp, _i32, _i32, _vp]),
     "ivftq_select_topn": (_i32, [_vp, _i64, _i32, _i32, _vp, _vp, _vp]),
-    "ivftq_probe_scratch_bytes": (_sz, [_i64, _i32]),
+    "ivftq_probe_scratch_bytes": (_sz, [_i64, _i32, _i32]),
+    "ivftq_assign_tc_scratch_bytes": (_sz, [_i64, _i32, _i32]),
+    "ivftq_assign_tc": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _sz, _vp]),
+    "ivftq_set_coarse_mode": (_i32, [_i32]),
+    "ivftq_coarse_tc_supported": (_i32, [_i32, _i32]),
+    "ivftq_coarse_prep_bytes": (_sz, [_i32, _i32]),
+    "ivftq_coarse_prepare": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "ivftq_probe": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
     "ivftq_scan_scratch_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "ivftq_scan_topk": (_i32, [C.POINTER(IvftqStore), _vp, _vp, _vp, _vp, _i64, _i32, _i32,

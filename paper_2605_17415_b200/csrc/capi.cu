@@ -151,8 +151,12 @@ extern "C" int ivftq_host_row_norms(const double* x, int64_t n, int dim, double*
   return 0;
 }
 
-extern "C" size_t ivftq_encode_scratch_bytes(int64_t n, int dim) {
-  return (size_t)2 * n * dim * sizeof(double) + 256;
+extern "C" size_t ivftq_assign_tc_scratch_bytes(int64_t n, int n_lists, int dim);
+
+extern "C" size_t ivftq_encode_scratch_bytes(int64_t n, int dim, int n_lists) {
+  const size_t a = (size_t)2 * n * dim * sizeof(double) + 256;
+  const size_t b = ivftq_assign_tc_scratch_bytes(n, n_lists, dim);
+  return a > b ? a : b;  // the assignment scratch is dead before the residuals
 }
 
 extern "C" int ivftq_encode(const void* x, int x_dtype, int64_t n, int dim, int bits,
@@ -161,7 +165,7 @@ extern "C" int ivftq_encode(const void* x, int x_dtype, int64_t n, int dim, int 
                             double* xn_out, int64_t* bad_row, int32_t* list_out,
                             uint16_t* norm_out, uint32_t* words_out, void* scratch,
                             size_t scratch_bytes, void* stream) {
-  if (scratch_bytes < ivftq_encode_scratch_bytes(n, dim)) {
+  if (scratch_bytes < ivftq_encode_scratch_bytes(n, dim, n_lists)) {
     set_error("encode: scratch too small");
     return IVFTQ_ERR_SCRATCH;
   }
@@ -172,7 +176,9 @@ extern "C" int ivftq_encode(const void* x, int x_dtype, int64_t n, int dim, int 
   if (flat) {
     IVFTQ_CHECK_CUDA(cudaMemsetAsync(list_out, 0, sizeof(int32_t) * n, (cudaStream_t)stream));
   } else {
-    if (int e = ivftq_assign(xn_out, centroids, n, n_lists, dim, list_out, stream)) return e;
+    if (int e = ivftq_assign_tc(xn_out, centroids, n, n_lists, dim, list_out, scratch,
+                                scratch_bytes, stream))
+      return e;
   }
   if (int e = ivftq_residuals(xn_out, centroids, list_out, n, dim, flat, resid, norm_out, stream))
     return e;

@@ -415,6 +415,84 @@ merge_kernel(const double* __restrict__ part_s, const int32_t* __restrict__ part
   }
 }
 
+// Warp-per-query merge for K <= 32*QS: a register queue sorted by (score
+// desc, id asc) with early rejection against its last entry; candidates
+// arrive in any order, so the insert position counts strictly better entries.
+template <int QS>
+__global__ void __launch_bounds__(256)
+merge_warp_kernel(const double* __restrict__ part_s, const int32_t* __restrict__ part_id,
+                  int64_t nq, int n_in, int K, int64_t* __restrict__ ids_out,
+                  double* __restrict__ s_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const double* ps = part_s + q * n_in;
+  const int32_t* pi = part_id + q * n_in;
+  long long qk[QS];
+  int qi[QS];
+#pragma unroll
+  for (int s = 0; s < QS; ++s) { qk[s] = LLONG_MIN; qi[s] = INT_MAX; }
+  int cnt = 0;
+  long long tk = LLONG_MIN;
+  int ti = INT_MAX;
+  const int tl = (K - 1) & 31, ts = (K - 1) >> 5;
+  for (int base = 0; base < n_in; base += 32) {
+    const int c = base + lane;
+    const int id = c < n_in ? pi[c] : INT_MAX;
+    const long long key = id != INT_MAX ? order_key(ps[c]) : LLONG_MIN;
+    unsigned m = __ballot_sync(kFull, id != INT_MAX && (cnt < K || key > tk || (key == tk && id < ti)));
+    while (m) {
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const long long k = __shfl_sync(kFull, key, src);
+      const int kid = __shfl_sync(kFull, id, src);
+      if (cnt == K && !(k > tk || (k == tk && kid < ti))) continue;
+      int p = 0;
+#pragma unroll
+      for (int s = 0; s < QS; ++s)
+        p += __popc(__ballot_sync(kFull, (s * 32 + lane) < cnt &&
+                                             (qk[s] > k || (qk[s] == k && qi[s] < kid))));
+      long long rk[QS];
+      int ri[QS];
+#pragma unroll
+      for (int s = 0; s < QS; ++s) {
+        rk[s] = __shfl_sync(kFull, qk[s], (lane + 31) & 31);
+        ri[s] = __shfl_sync(kFull, qi[s], (lane + 31) & 31);
+      }
+#pragma unroll
+      for (int s = QS - 1; s >= 0; --s) {
+        const int pos = s * 32 + lane;
+        long long pk = rk[s];
+        int pv = ri[s];
+        if (lane == 0) {
+          pk = s > 0 ? rk[s > 0 ? s - 1 : 0] : LLONG_MIN;
+          pv = s > 0 ? ri[s > 0 ? s - 1 : 0] : INT_MAX;
+        }
+        if (pos > p) { qk[s] = pk; qi[s] = pv; }
+        else if (pos == p) { qk[s] = k; qi[s] = kid; }
+      }
+      cnt = min(cnt + 1, K);
+      if (cnt == K) {
+        long long t = qk[0];
+        int u = qi[0];
+#pragma unroll
+        for (int s = 1; s < QS; ++s) if (s == ts) { t = qk[s]; u = qi[s]; }
+        tk = __shfl_sync(kFull, t, tl);
+        ti = __shfl_sync(kFull, u, tl);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < QS; ++s) {
+    const int pos = s * 32 + lane;
+    if (pos < K) {
+      const bool have = pos < cnt;
+      ids_out[q * K + pos] = have ? (int64_t)qi[s] : -1;
+      s_out[q * K + pos] = have ? key_value(qk[s]) : -INFINITY;
+    }
+  }
+}
+
 // Exact f64 re-score of candidates against the raw store (index.py:470-473).
 __global__ void __launch_bounds__(128)
 rerank_kernel(const float* __restrict__ raw, const double* __restrict__ qn,
@@ -488,16 +566,51 @@ extern "C" int ivftq_select_topn(const double* scores, int64_t rows, int cols, i
   return check_launch("select_topn");
 }
 
-extern "C" size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists) {
+extern bool g_probe_tc_force;
+int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, int dim,
+             int n_p, int32_t* probe_out, double* coarse_out, void* scratch,
+             size_t scratch_bytes, cudaStream_t s);
+extern "C" size_t ivftq_probe_tc_scratch_bytes(int64_t nq, int n_lists, int dim);
+static bool probe_tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("IVFTQ_PROBE_TC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1 || g_probe_tc_force;
+}
+
+extern "C" size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists, int dim) {
+  const size_t t = ivftq_probe_tc_scratch_bytes(nq, n_lists, dim);
+  const size_t f = (size_t)nq * n_lists * sizeof(double) + 256;
+  return t > f ? t : f;
+}
+
+static size_t probe_f64_scratch_bytes(int64_t nq, int n_lists) {
   return (size_t)nq * n_lists * sizeof(double) + 256;
 }
 
 extern "C" int ivftq_probe(const double* qn, const float* centroids, int64_t nq, int n_lists,
                            int dim, int n_p, int32_t* probe_out, double* coarse_out,
                            void* scratch, size_t scratch_bytes, void* stream) {
-  if (scratch_bytes < ivftq_probe_scratch_bytes(nq, n_lists)) {
+  if (scratch_bytes < probe_f64_scratch_bytes(nq, n_lists)) {
     set_error("probe: scratch too small");
     return IVFTQ_ERR_SCRATCH;
+  }
+  if (n_p < 1 || n_p > n_lists) {
+    set_error("probe: n_p=%d must be in [1, n_lists=%d]", n_p, n_lists);
+    return IVFTQ_ERR_ARG;
+  }
+  if (nq == 0) return 0;
+  // Probes take the f64 GEMM + exact select by default: every selected probe
+  // needs its exact f64 coarse score, and re-scoring ~n_p gathered centroid
+  // rows per query (no reuse across queries) measured slower than the dense
+  // f64 GEMM at C2 (325 us vs 167 us). IVFTQ_PROBE_TC=1 selects the tcgen05
+  // path (identical results; tests exercise both).
+  if (probe_tc_enabled()) {
+    const int e = probe_tc(qn, centroids, nq, n_lists, dim, n_p, probe_out, coarse_out, scratch,
+                           scratch_bytes, (cudaStream_t)stream);
+    if (e != IVFTQ_ERR_UNSUPPORTED) return e;
   }
   double* S = (double*)scratch;
   if (int e = ivftq_gemm_nt(qn, centroids, IVFTQ_F32, nq, n_lists, dim, S, IVFTQ_F64, stream))
@@ -526,8 +639,14 @@ int merge_smem_opt_in(int K) {
 }
 void launch_merge(const double* part_s, const int32_t* part_id, int64_t nq, int n_in, int K,
                   int64_t* ids_out, double* s_out, cudaStream_t s) {
-  merge_kernel<<<(unsigned)nq, 128, BlockTopK::bytes(topk_cap(K, 128)), s>>>(
-      part_s, part_id, n_in, K, ids_out, s_out);
+  const unsigned wb = (unsigned)((nq + 7) / 8);
+  if (K <= 32)
+    merge_warp_kernel<1><<<wb, 256, 0, s>>>(part_s, part_id, nq, n_in, K, ids_out, s_out);
+  else if (K <= 64)
+    merge_warp_kernel<2><<<wb, 256, 0, s>>>(part_s, part_id, nq, n_in, K, ids_out, s_out);
+  else
+    merge_kernel<<<(unsigned)nq, 128, BlockTopK::bytes(topk_cap(K, 128)), s>>>(
+        part_s, part_id, n_in, K, ids_out, s_out);
 }
 }  // namespace ivftq
 

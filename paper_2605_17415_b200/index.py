@@ -227,7 +227,7 @@ class IvfTqIndex:
         lids = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
         nrm = torch.empty(max(n, 1), dtype=torch.int16, device=dev)
         words = torch.empty((max(n, 1), W), dtype=torch.int32, device=dev)
-        sb = self._lib.ivftq_encode_scratch_bytes(n, d)
+        sb = self._lib.ivftq_encode_scratch_bytes(n, d, self.partition.n_lists)
         scratch = torch.empty(sb, dtype=torch.uint8, device=dev)
         _lib.check(self._lib.ivftq_encode(
             xt.data_ptr(), code, n, d, cfg.bits, int(cfg.use_sign_bit), int(cfg.flat),
@@ -447,7 +447,7 @@ class IvfTqIndex:
         s = _lib.stream_ptr()
         probe = torch.empty((max(nq, 1), n_p), dtype=torch.int32, device=dev)
         coarse = torch.empty((max(nq, 1), n_p), dtype=torch.float64, device=dev)
-        pb = self._lib.ivftq_probe_scratch_bytes(nq, L)
+        pb = self._lib.ivftq_probe_scratch_bytes(nq, L, d)
         pscr = torch.empty(pb, dtype=torch.uint8, device=dev)
         _lib.check(self._lib.ivftq_probe(qn.data_ptr(), self._cent.data_ptr(), nq, L, d, n_p,
                                          probe.data_ptr(), coarse.data_ptr(), pscr.data_ptr(),

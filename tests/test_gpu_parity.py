@@ -117,7 +117,7 @@ def test_probes_identical(golden):
     L = _lib.lib()
     probe = torch.empty((nq, 64), dtype=torch.int32, device="cuda")
     coarse = torch.empty((nq, 64), dtype=torch.float64, device="cuda")
-    sb = L.ivftq_probe_scratch_bytes(nq, 64)
+    sb = L.ivftq_probe_scratch_bytes(nq, 64, 128)
     scr = torch.empty(sb, dtype=torch.uint8, device="cuda")
     _lib.check(L.ivftq_probe(qn.data_ptr(), idx._cent.data_ptr(), nq, 64, 128, 64,
                              probe.data_ptr(), coarse.data_ptr(), scr.data_ptr(), sb,
@@ -430,3 +430,85 @@ def test_train_partition_device_matches_reference(golden, name):
     np.testing.assert_allclose(p.centroids, g["centroids"], rtol=0, atol=1e-6)
     sizes = np.array([len(m) for m in p.lists])
     assert sizes.sum() == len(x)
+
+
+def _coarse_case(seed, n, L, d, dup=True):
+    rng = np.random.default_rng(seed)
+    c = rng.standard_normal((L, d))
+    if dup and L >= 8:
+        c[L // 2] = c[1]            # exact duplicate centroid: ties -> lower list
+        c[L - 1] = c[1] * (1 + 1e-9)  # near-duplicate inside the guard band
+    c = (c / np.linalg.norm(c, axis=1)[:, None]).astype(np.float32)
+    x = rng.standard_normal((n, d))
+    m = min(5, n, L)
+    x[:m] = c[:m]  # rows sitting on centroids
+    x /= np.linalg.norm(x, axis=1)[:, None]
+    return x, c
+
+
+def _with_mode(L, mode, fn):
+    L.ivftq_set_coarse_mode(mode)
+    try:
+        return fn()
+    finally:
+        L.ivftq_set_coarse_mode(0)
+
+
+@pytest.mark.parametrize("n,L,d,n_p", [(300, 64, 32, 8), (1000, 1024, 128, 64), (257, 300, 96, 33),
+                                       (128, 130, 200, 1), (64, 4096, 96, 128), (10, 16, 7, 16)])
+def test_coarse_tc_probes_identical_to_f64(n, L, d, n_p):
+    """Tensor-core coarse scores + exact guard band == the f64 GEMM path:
+    identical probe lists (stable order) and bit-identical coarse values."""
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+
+    lib = _lib.lib()
+    x, c = _coarse_case(n + L + d, n, L, d)
+    xd = torch.from_numpy(x).cuda()
+    cd = torch.from_numpy(c).cuda()
+
+    def run():
+        probe = torch.empty((n, n_p), dtype=torch.int32, device="cuda")
+        coarse = torch.empty((n, n_p), dtype=torch.float64, device="cuda")
+        sb = lib.ivftq_probe_scratch_bytes(n, L, d)
+        scr = torch.empty(sb, dtype=torch.uint8, device="cuda")
+        _lib.check(lib.ivftq_probe(xd.data_ptr(), cd.data_ptr(), n, L, d, n_p, probe.data_ptr(),
+                                   coarse.data_ptr(), scr.data_ptr(), sb, _lib.stream_ptr()))
+        torch.cuda.synchronize()
+        return probe.cpu().numpy(), coarse.cpu().numpy()
+
+    assert lib.ivftq_coarse_tc_supported(d, L) == 1
+    p_tc, c_tc = _with_mode(lib, 2, run)
+    p_64, c_64 = _with_mode(lib, 1, run)
+    np.testing.assert_array_equal(p_tc, p_64)
+    np.testing.assert_array_equal(c_tc, c_64)
+    # and against numpy's stable argsort of the f64 scores
+    s = x @ c.astype(np.float64).T
+    want = np.argsort(-s, axis=1, kind="stable")[:, :n_p]
+    np.testing.assert_array_equal(p_tc, want)
+
+
+@pytest.mark.parametrize("n,L,d", [(5000, 1024, 128), (777, 33, 64), (300, 4096, 96),
+                                   (200, 8, 200), (50, 3, 5)])
+def test_assign_tc_identical_to_f64(n, L, d):
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+
+    lib = _lib.lib()
+    x, c = _coarse_case(n * 7 + L, n, L, d)
+    xd = torch.from_numpy(x).cuda()
+    cd = torch.from_numpy(c).cuda()
+    out_tc = torch.empty(n, dtype=torch.int32, device="cuda")
+    out_64 = torch.empty(n, dtype=torch.int32, device="cuda")
+    sb = lib.ivftq_assign_tc_scratch_bytes(n, L, d)
+    scr = torch.empty(sb, dtype=torch.uint8, device="cuda")
+    _lib.check(lib.ivftq_assign_tc(xd.data_ptr(), cd.data_ptr(), n, L, d, out_tc.data_ptr(),
+                                   scr.data_ptr(), sb, _lib.stream_ptr()))
+    _lib.check(lib.ivftq_assign(xd.data_ptr(), cd.data_ptr(), n, L, d, out_64.data_ptr(),
+                                _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(out_tc.cpu().numpy(), out_64.cpu().numpy())
+    np.testing.assert_array_equal(out_tc.cpu().numpy(),
+                                  np.argmax(x @ c.astype(np.float64).T, axis=1))
