@@ -58,16 +58,18 @@ constexpr int kDecWarps = 8;
 constexpr int kEpiWarp0 = 10;    // epilogue warps 10..17
 constexpr int kEpiWarps = 8;
 constexpr int kSchedWarp = kEpiWarp0 + kEpiWarps;  // 18: item scheduler
-constexpr int kThreads = 32 * (kSchedWarp + 1);      // 608
+constexpr int kAbWarp0 = kSchedWarp + 1;             // 19..22: A-operand builders
+constexpr int kThreads = 32 * (kAbWarp0 + 4);        // 736
 constexpr int kItemSlots = 2;    // item-record ring (scheduler -> producer)
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
 constexpr int kNS = 4;           // stage ring depth (power of two)
 constexpr int kMeta = 4;         // tile-record ring depth (power of two)
-constexpr int kAcc = 4;          // TMEM accumulator ring depth (power of two)
-constexpr int kNV = 64;          // vectors per tile (MMA N)
-// TMEM budget: kAcc accumulators of kNV columns + the A operand (DP columns)
-constexpr int kMaxDim = 512 - kAcc * kNV;
+constexpr int kAccMax = 4;       // TMEM accumulator ring depth bound (power of two)
+// Tile shapes (vectors per tile = MMA N, accumulator ring depth): 128 x 2 when
+// shared memory and TMEM allow, else 64 x 4. TMEM budget: nAcc accumulators of
+// NV columns + nA A-operand buffers of DP columns <= 512.
+constexpr int kMaxDim = 256;
 
 
 // control record of one tile in a stage slot
@@ -158,6 +160,7 @@ struct Params {
   const uint32_t* q_hi;    // [nq][DP/2] rotated query rows, fp16 hi halves (x 2^14), packed pairs
   const uint32_t* q_lo;    // [nq][DP/2] matching lo halves
   int n_p, k, d, DP, NV, NS;
+  int nAcc;         // TMEM accumulator ring depth (power of two, <= kAccMax)
   int nA;           // A-operand buffers in TMEM (2 when they fit: next item's
                     // queries are written while the current item's MMAs run)
   float t_scale;    // 2^eT
@@ -300,7 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   const int W = P.st.words_per_vec, DP = P.DP, d = P.d, NCH = DP / 8;
   // TMEM columns: kAcc accumulators of NV columns, then the A operand
   // (Qhi, Qlo: DP/2 columns each)
-  const uint32_t a_col = kAcc * NV;
+  const int nAcc = P.nAcc;
+  const uint32_t a_col = nAcc * NV;
   const uint32_t need = a_col + P.nA * DP;
   const uint32_t tmem_cols = need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
   const Layout& Lo = P.lo;  // kernel-parameter space: no per-use recomputation
@@ -312,8 +316,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   uint64_t* st_empty = bars + 8;       // [NS] decoders + epilogue -> producer
   uint64_t* op_full = bars + 16;       // [2] decoders -> MMA
   uint64_t* op_empty = bars + 18;      // [2] MMA commit -> decoders
-  uint64_t* acc_full = bars + 36;      // [kAcc] MMA commit -> epilogue
-  uint64_t* acc_empty = bars + 40;     // [kAcc] epilogue -> MMA
+  uint64_t* acc_full = bars + 36;      // [nAcc] MMA commit -> epilogue
+  uint64_t* acc_empty = bars + 40;     // [nAcc] epilogue -> MMA
   uint64_t* a_full = bars + 20;        // [nA] decoders -> MMA (A operand built)
   uint64_t* a_empty = bars + 22;       // [nA] MMA commit -> decoders (A operand free)
   uint64_t* meta_full = bars + 26;     // [kMeta] decoders -> MMA/epilogue (tile record)
@@ -341,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       sm100::mbar_init(&op_full[b], kDecWarps);
       sm100::mbar_init(&op_empty[b], 1);
     }
-    for (int b = 0; b < kAcc; ++b) {
+    for (int b = 0; b < kAccMax; ++b) {
       sm100::mbar_init(&acc_full[b], 1);
       sm100::mbar_init(&acc_empty[b], kEpiWarps);
     }
@@ -350,12 +354,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       sm100::mbar_init(&meta_empty[m], kEpiWarps);
     }
     for (int b = 0; b < 2; ++b) {
-      sm100::mbar_init(&a_full[b], kDecWarps);
+      sm100::mbar_init(&a_full[b], 4);
       sm100::mbar_init(&a_empty[b], 1);
     }
     for (int b = 0; b < kItemSlots; ++b) {
       sm100::mbar_init(&it_full[b], 1);
-      sm100::mbar_init(&it_empty[b], 1);
+      sm100::mbar_init(&it_empty[b], 5);  // producer + 4 A builders
     }
     sm100::mbar_fence_init();
   }
@@ -374,12 +378,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0, j = 0;
     for (;;) {
       const int slot = j % kItemSlots;
-      sm100::mbar_wait_sleep(&it_full[slot], (j / kItemSlots) & 1);
+      sm100::mbar_wait_sleep<512>(&it_full[slot], (j / kItemSlots) & 1);
       const ItemRec* rec = (const ItemRec*)(smem + Lo.items + slot * Lo.item_bytes);
       const int l = rec->list;
       if (l < 0) {
         const int s = t % NS;
-        if (t >= (uint32_t)NS) sm100::mbar_wait_sleep(&st_empty[s], ((t / NS) - 1) & 1);
+        if (t >= (uint32_t)NS) sm100::mbar_wait_sleep<512>(&st_empty[s], ((t / NS) - 1) & 1);
         if (lane == 0) {
           Ctrl* c = (Ctrl*)(stage(s) + Lo.st_ctrl);
           c->list = -1;
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
                                  : LLONG_MIN;
         }
         const int s = t % NS;
-        if (t >= (uint32_t)NS) sm100::mbar_wait_sleep(&st_empty[s], ((t / NS) - 1) & 1);
+        if (t >= (uint32_t)NS) sm100::mbar_wait_sleep<512>(&st_empty[s], ((t / NS) - 1) & 1);
         unsigned char* sp = stage(s);
         int* qrow = (int*)(sp + Lo.st_qrow);
         float* qb = (float*)(qrow + kM);
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const int slot = j % kItemSlots;
       ItemRec* rec = (ItemRec*)(smem + Lo.items + slot * Lo.item_bytes);
       if (item >= n_items) {
-        if (j >= (uint32_t)kItemSlots) sm100::mbar_wait_sleep(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
+        if (j >= (uint32_t)kItemSlots) sm100::mbar_wait_sleep<512>(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
         if (lane == 0) {
           rec->list = -1;
           mbar_arrive(&it_full[slot]);
@@ -502,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           }
         }
       }
-      if (j >= (uint32_t)kItemSlots) sm100::mbar_wait_sleep(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
+      if (j >= (uint32_t)kItemSlots) sm100::mbar_wait_sleep<512>(&it_empty[slot], ((j / kItemSlots) - 1) & 1);
 #pragma unroll
       for (int q = 0; q < kM / 32; ++q) {
         rec->prow[q * 32 + lane] = prow[q];
@@ -520,6 +524,56 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       if (lane == 0) mbar_arrive(&it_full[slot]);
       ++j;
     }
+  } else if (warp >= kAbWarp0) {
+    // ================= A-operand builders ========================================
+    // One item ahead of the MMA (A is double-buffered in TMEM when it fits):
+    // warp w writes TMEM lane quadrant w%4 -- the item's query rows, fp16 hi in
+    // the first DP/2 columns and lo in the next, straight from the pre-split
+    // rows -- once the MMAs of the item that last used the buffer are done.
+    const int quad = warp & 3;
+    uint32_t j = 0;
+    for (;;) {
+      const int slot = j % kItemSlots;
+      sm100::mbar_wait_sleep<512>(&it_full[slot], (j / kItemSlots) & 1);
+      const ItemRec* rec = (const ItemRec*)(smem + Lo.items + slot * Lo.item_bytes);
+      const int l = rec->list;
+      const int pi = l >= 0 ? rec->prow[quad * 32 + lane] : -1;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&it_empty[slot]);
+      if (l < 0) break;
+      const uint32_t ab_ = j % P.nA;
+      if (j >= (uint32_t)P.nA) sm100::mbar_wait_sleep<512>(&a_empty[ab_], ((j / P.nA) - 1) & 1);
+      sm100::tc_fence_after();
+      const int64_t qo = (int64_t)(pi >= 0 ? pi / P.n_p : 0) * (DP / 2);
+#pragma unroll 1
+      for (int part = 0; part < 2; ++part) {
+        const uint4* src = (const uint4*)((part ? P.q_lo : P.q_hi) + qo);
+        const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + a_col + ab_ * DP + part * (DP / 2);
+#pragma unroll 1
+        for (int c16 = 0; c16 < DP / 2; c16 += 64) {
+          uint32_t v[4][16];
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh)
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const bool ok = pi >= 0 && c16 + hh * 16 < DP / 2;
+              const uint4 w4 = ok ? __ldg(src + (c16 + hh * 16) / 4 + x) : make_uint4(0, 0, 0, 0);
+              v[hh][4 * x] = w4.x;
+              v[hh][4 * x + 1] = w4.y;
+              v[hh][4 * x + 2] = w4.z;
+              v[hh][4 * x + 3] = w4.w;
+            }
+#pragma unroll
+          for (int hh = 0; hh < 4; ++hh)
+            if (c16 + hh * 16 < DP / 2) sm100::tmem_st16(ta + c16 + hh * 16, v[hh]);
+        }
+      }
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_full[ab_]);
+      ++j;
+    }
   } else if (warp == kMmaWarp) {
     // ================= MMA issuer ===============================================
     const uint32_t idesc = sm100::idesc_f16_f32(kM, NV);
@@ -528,17 +582,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0, u = 0;
     for (;;) {
       const int ob = t & 1;
-      sm100::mbar_wait(&op_full[ob], (t >> 1) & 1);
+      sm100::mbar_wait_sleep<32>(&op_full[ob], (t >> 1) & 1);
       const Ctrl c = *(const Ctrl*)(meta(t & (kMeta - 1)));
-      const int ab = t & (kAcc - 1);
-      if (t >= (uint32_t)kAcc) sm100::mbar_wait(&acc_empty[ab], ((t / kAcc) - 1) & 1);
+      const int ab = t & (nAcc - 1);
+      if (t >= (uint32_t)nAcc) sm100::mbar_wait_sleep<32>(&acc_empty[ab], ((t / nAcc) - 1) & 1);
       if (c.list < 0) {
         if (lane == 0) mbar_arrive(&acc_full[ab]);
         break;
       }
       if (c.tile == 0) {
         abuf = u % P.nA;
-        sm100::mbar_wait(&a_full[abuf], (u / P.nA) & 1);
+        sm100::mbar_wait_sleep<32>(&a_full[abuf], (u / P.nA) & 1);
         ++u;
       }
       const uint32_t qhi_t = tmem + a_col + abuf * DP, qlo_t = qhi_t + DP / 2;  // A in TMEM
@@ -614,50 +668,6 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         __syncwarp();
         if (lane == 0) mbar_arrive(&op_full[ob]);
         break;
-      }
-      if (c.tile == 0) {
-        // A operand for the new item: wait until the previous item's MMAs are done
-        // A lives in TMEM: lane = query row, 2 fp16 per 32-bit column along K.
-        // Decoder warp w writes TMEM lane quadrant w%4; warps 2..5 the hi
-        // halves, 6..9 the lo halves, straight from the pre-split rows.
-        const uint32_t ab_ = u % P.nA;
-        if (u >= (uint32_t)P.nA) sm100::mbar_wait_sleep(&a_empty[ab_], ((u / P.nA) - 1) & 1);
-        DTRACE(2);
-        sm100::tc_fence_after();
-        {
-          const int part = (warp - kDecWarp0) >> 2;  // 0 = hi, 1 = lo
-          const int rrow = (warp & 3) * 32 + lane;
-          const int pi = ((const int*)(sp + Lo.st_qrow))[rrow];
-          const uint4* src = (const uint4*)((part ? P.q_lo : P.q_hi) +
-                                            (int64_t)(pi >= 0 ? pi / P.n_p : 0) * (DP / 2));
-          const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + a_col + ab_ * DP +
-                              part * (DP / 2);
-          // four 16-column chunks (a whole DP<=128 row) in flight per round trip
-#pragma unroll 1
-          for (int c16 = 0; c16 < DP / 2; c16 += 64) {
-            uint32_t v[4][16];
-#pragma unroll
-            for (int hh = 0; hh < 4; ++hh)
-#pragma unroll
-              for (int x = 0; x < 4; ++x) {
-                const bool ok = pi >= 0 && c16 + hh * 16 < DP / 2;
-                const uint4 w4 = ok ? __ldg(src + (c16 + hh * 16) / 4 + x) : make_uint4(0, 0, 0, 0);
-                v[hh][4 * x] = w4.x;
-                v[hh][4 * x + 1] = w4.y;
-                v[hh][4 * x + 2] = w4.z;
-                v[hh][4 * x + 3] = w4.w;
-              }
-#pragma unroll
-            for (int hh = 0; hh < 4; ++hh)
-              if (c16 + hh * 16 < DP / 2) sm100::tmem_st16(ta + c16 + hh * 16, v[hh]);
-          }
-          sm100::tmem_st_wait();
-        }
-        sm100::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&a_full[ab_]);
-        DTRACE(3);
-        ++u;
       }
       // ---- decode this tile's codes into the B operand ----------------------------
       const uint32_t* cw = (const uint32_t*)(sp + Lo.st_codes);
@@ -750,8 +760,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0, tag = 0;
     const int cols = NV / 2;
     for (;;) {
-      const int ab = t & (kAcc - 1), ms = t & (kMeta - 1);
-      sm100::mbar_wait_sleep(&acc_full[ab], (t / kAcc) & 1);
+      const int ab = t & (nAcc - 1), ms = t & (kMeta - 1);
+      sm100::mbar_wait_sleep(&acc_full[ab], (t / nAcc) & 1);
       sm100::mbar_wait_sleep(&meta_full[ms], (t / kMeta) & 1);
       const unsigned char* mp = meta(ms);
       const Ctrl c = *(const Ctrl*)mp;
@@ -1072,12 +1082,20 @@ static const size_t kSmemLimit = 227 * 1024;
 // Widest vector tile, then deepest stage ring, that fits in shared memory.
 static int kmax_for(int depth) { return depth <= 10 ? 10 : 32; }
 
-static bool pick_tile(int DP, int W, int C, int kmax, int* nv, int* ns) {
+static bool pick_tile(int DP, int W, int C, int kmax, int* nv, int* ns, int* nacc = nullptr) {
   if (DP > kMaxDim) return false;
-  if (make_layout(kNV, kNS, DP, W, C, kmax).total + 1024 > kSmemLimit) return false;
-  *nv = kNV;
-  *ns = kNS;
-  return true;
+  static const int shapes[2][2] = {{128, 2}, {64, 4}};  // (NV, nAcc), widest first
+  const char* force = getenv("IVFTQ_SCAN_NV");
+  for (const auto& sh : shapes) {
+    if (force && atoi(force) != sh[0]) continue;
+    if (sh[0] * sh[1] + DP > 512) continue;  // one A buffer at least
+    if (make_layout(sh[0], kNS, DP, W, C, kmax).total + 1024 > kSmemLimit) continue;
+    *nv = sh[0];
+    *ns = kNS;
+    if (nacc) *nacc = sh[1];
+    return true;
+  }
+  return false;
 }
 
 extern "C" int ivftq_scan_tc_supported(int dim, int bits, int depth) {
@@ -1151,7 +1169,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   }
   Params P{};
   const int kmax = kmax_for(depth);
-  pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS);
+  pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS, &P.nAcc);
   P.st = *st;
   P.coarse = coarse;
   P.qrot = qrot;
@@ -1177,7 +1195,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   P.k = depth;
   P.d = st->dim;
   P.DP = DP;
-  P.nA = (kAcc * kNV + 2 * DP <= 512) ? 2 : 1;
+  P.nA = (P.nAcc * P.NV + 2 * DP <= 512) ? 2 : 1;
   // Every Lloyd-Max level satisfies |T| < 5/sqrt(d) < 4, so 2^12 keeps the
   // scaled table below 2^14 and its hi/lo halves in the fp16 normal range.
   const int eT = 12;

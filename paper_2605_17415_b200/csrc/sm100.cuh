@@ -45,6 +45,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Same for warps off the critical path: between polls the warp sleeps ~64 ns,
 // so idle roles stop taking issue slots from the busy warps of their SM
 // sub-partition.
+template <int NS = 64>
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -52,11 +53,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "LAB_WAITS:\n"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n"
       "@P1 bra DONES;\n"
-      "nanosleep.u32 64;\n"
+      "nanosleep.u32 %3;\n"
       "bra LAB_WAITS;\n"
       "DONES:\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000)
+      "r"(parity), "r"(1000000), "n"(NS)
       : "memory");
 }
 
