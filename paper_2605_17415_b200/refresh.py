@@ -89,7 +89,7 @@ def reconstruct_vector(index: IvfTqIndex, internal_id: int) -> np.ndarray:
 def _stratified_sample_ids(lists, n, n_lists, sample_size, rng):
     picked = []
     for members in lists:
-        if not members:
+        if len(members) == 0:
             continue
         take = max(1, int(np.ceil(sample_size * len(members) / n)))
         take = min(take, len(members))
@@ -149,7 +149,12 @@ def refresh(index: IvfTqIndex, policy: RefreshPolicy, kmeans_device: str = "cpu"
     used_raw = bool(policy.use_raw_if_available and index._raw is not None)
 
     rng = np.random.default_rng(policy.seed)
-    sample_ids = _stratified_sample_ids(index.partition.lists, n, n_lists, sample_size, rng)
+    # per-list members in ascending id order (what partition.lists holds,
+    # refresh.py:115-121), as arrays: no Python list of n ints at 10M scale
+    lids = index.list_ids
+    order = np.argsort(lids, kind="stable")
+    members = np.split(order, np.cumsum(np.bincount(lids, minlength=n_lists))[:-1])
+    sample_ids = _stratified_sample_ids(members, n, n_lists, sample_size, rng)
     dev = index.device
     if centroids is None:
         sid = torch.from_numpy(sample_ids).to(dev)
