@@ -113,6 +113,17 @@ __global__ void prep_c64_kernel(const float* __restrict__ c, int64_t n, double* 
   if (i < n) out[i] = (double)c[i];
 }
 
+__device__ __forceinline__ float pick16f(const float (&v)[16], int j) {
+  float a[8], b[4], c[2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = (j & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) b[i] = (j & 2) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) c[i] = (j & 4) ? b[2 * i + 1] : b[2 * i];
+  return (j & 8) ? c[1] : c[0];
+}
+
 __device__ __forceinline__ uint64_t akey(float v, int id) {
   uint32_t b = __float_as_uint(v + 0.0f);
   b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
@@ -261,15 +272,31 @@ coarse_tc_kernel(const double* __restrict__ X, int64_t n, int d, int DP, int L, 
           }
         }
         if (top_v) {
+          // only columns beating the row's current 4th best reach the insert
+          // (columns arrive in ascending order, so an equal value never does);
+          // the warp steps max-over-lanes times per 16-column window
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const uint64_t key = col0 + e < L ? akey(f[e], col0 + e) : 0ull;
-            bool g[kTopA];
+          for (int h = 0; h < 32; h += 16) {
+            const float kth = best[kTopA - 1] ? akey_v(best[kTopA - 1]) : -INFINITY;
+            uint32_t m = 0;
 #pragma unroll
-            for (int p = 0; p < kTopA; ++p) g[p] = key > best[p];
+            for (int e = 0; e < 16; ++e)
+              m |= (col0 + h + e < L && f[h + e] > kth ? 1u : 0u) << e;
+            while (__any_sync(kFull, m != 0)) {
+              const int j = (__ffs(m) - 1) & 15;
+              float w[16];
 #pragma unroll
-            for (int p = kTopA - 1; p > 0; --p) best[p] = g[p] ? (g[p - 1] ? best[p - 1] : key) : best[p];
-            best[0] = g[0] ? key : best[0];
+              for (int e = 0; e < 16; ++e) w[e] = f[h + e];
+              const uint64_t key = m ? akey(pick16f(w, j), col0 + h + j) : 0ull;
+              m &= m - 1;
+              bool g[kTopA];
+#pragma unroll
+              for (int p = 0; p < kTopA; ++p) g[p] = key > best[p];
+#pragma unroll
+              for (int p = kTopA - 1; p > 0; --p)
+                best[p] = g[p] ? (g[p - 1] ? best[p - 1] : key) : best[p];
+              best[0] = g[0] ? key : best[0];
+            }
           }
         }
       }
