@@ -795,7 +795,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
           // rows past the item's queries (zero A rows) take nothing
           const float thr = row < c.nqt ? fmaxf(fmaxf(top.kth(), oth), bnd) : INFINITY;
           float res[kDrain];
-          uint32_t m = 0;
+          float mx = -INFINITY;  // fmaxf drops the NaN padding columns
 #pragma unroll
           for (int e = 0; e < kDrain; e += 4) {
             const float4 f4 = *(const float4*)(nsc + c0 + cc + h + e);
@@ -803,10 +803,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
 #pragma unroll
             for (int x = 0; x < 4; ++x) {
               res[e + x] = __fmul_rn(__uint_as_float(r[h + e + x]), ns[x]);
-              m |= (res[e + x] >= thr ? 1u : 0u) << (e + x);  // NaN padding never passes
+              mx = fmaxf(mx, res[e + x]);
             }
           }
           ETRACE(1 + 3 * (h / kDrain), clock64());
+          // one compare per window; the per-column mask only when some lane
+          // of the warp has a survivor in it
+          uint32_t m = 0;
+          if (__any_sync(kFull, mx >= thr)) {
+#pragma unroll
+            for (int e = 0; e < kDrain; ++e) m |= (res[e] >= thr ? 1u : 0u) << e;  // NaN never passes
+          }
           if (__any_sync(kFull, m != 0)) {
             ETRACE(3 + 3 * (h / kDrain), __popc(m));
             do {
