@@ -160,7 +160,7 @@ struct Params {
   const uint32_t* q_hi;    // [nq][DP/2] rotated query rows, fp16 hi halves (x 2^14), packed pairs
   const uint32_t* q_lo;    // [nq][DP/2] matching lo halves
   int n_p, k, d, DP, NV, NS;
-  int nAcc;         // TMEM accumulator ring depth (power of two, <= kAccMax)
+  int nAcc;         // TMEM accumulator ring depth (<= kAccMax)
   int nA;           // A-operand buffers in TMEM (2 when they fit: next item's
                     // queries are written while the current item's MMAs run)
   float t_scale;    // 2^eT
@@ -230,25 +230,34 @@ struct RegTopK {
 constexpr int gcd_c(int a, int b) { return b ? gcd_c(b, a % b) : a; }
 
 constexpr int kTraceTiles = 4096;
+// Timeline instrumentation (CTA 0, lane 0 of the role's first warp), compiled
+// in only for the trace build (make trace -> libivftq_b200_trace.so, used with
+// IVFTQ_LIB=... and IVFTQ_TRACE=<file>): even untaken, the checks cost ~5 %.
+#ifdef IVFTQ_TRACE_BUILD
 #define TRACE(slot)                                                              \
   do {                                                                           \
     if (P.trace && blockIdx.x == 0 && lane == 0 && t < (uint32_t)kTraceTiles)    \
       P.trace[t * 8 + (slot)] = clock64();                                       \
   } while (0)
-// epilogue-internal timeline (warp kEpiWarp0, lane 0 of CTA 0)
+// epilogue-internal timeline (warp kEpiWarp0)
 #define ETRACE(slot, val)                                                        \
   do {                                                                           \
     if (P.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarp0 &&          \
         t < (uint32_t)kTraceTiles)                                               \
       P.trace[8 * kTraceTiles + t * 8 + (slot)] = (val);                         \
   } while (0)
-// decoder-internal timeline (warp kDecWarp0, lane 0 of CTA 0)
+// decoder-internal timeline (warp kDecWarp0)
 #define DTRACE(slot)                                                             \
   do {                                                                           \
     if (P.trace && blockIdx.x == 0 && lane == 0 && warp == kDecWarp0 &&          \
         t < (uint32_t)kTraceTiles)                                               \
       P.trace[16 * kTraceTiles + t * 8 + (slot)] = clock64();                    \
   } while (0)
+#else
+#define TRACE(slot) do {} while (0)
+#define ETRACE(slot, val) do {} while (0)
+#define DTRACE(slot) do {} while (0)
+#endif
 
 // f64 <-> int64 key preserving order, so atomicMax works on scores
 __device__ __forceinline__ long long dkey(double x) {
@@ -584,7 +593,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const int ob = t & 1;
       sm100::mbar_wait_sleep<32>(&op_full[ob], (t >> 1) & 1);
       const Ctrl c = *(const Ctrl*)(meta(t & (kMeta - 1)));
-      const int ab = t & (nAcc - 1);
+      const int ab = t % nAcc;
       if (t >= (uint32_t)nAcc) sm100::mbar_wait_sleep<32>(&acc_empty[ab], ((t / nAcc) - 1) & 1);
       if (c.list < 0) {
         if (lane == 0) mbar_arrive(&acc_full[ab]);
@@ -760,15 +769,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     uint32_t t = 0, tag = 0;
     const int cols = NV / 2;
     for (;;) {
-      const int ab = t & (nAcc - 1), ms = t & (kMeta - 1);
+      const int ab = t % nAcc, ms = t & (kMeta - 1);
       sm100::mbar_wait_sleep(&acc_full[ab], (t / nAcc) & 1);
       sm100::mbar_wait_sleep(&meta_full[ms], (t / kMeta) & 1);
       const unsigned char* mp = meta(ms);
       const Ctrl c = *(const Ctrl*)mp;
       if (c.list < 0) break;
       if (warp == kEpiWarp0) TRACE(5);
+#ifdef IVFTQ_TRACE_BUILD
       if (P.trace && blockIdx.x == 0 && lane == 0 && warp == kEpiWarp0 && t < (uint32_t)kTraceTiles)
         P.trace[t * 8 + 7] = c.tile | (c.ntiles << 12) | ((long long)c.nqt << 24);
+#endif
       const int pi = ((const int*)(mp + Lo.m_qrow))[row];
       const float bnd = ((const float*)(mp + Lo.m_qrow))[kM + row];
       if (c.tile == 0) {
@@ -785,7 +796,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         uint32_t r[32];
         sm100::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
         sm100::tmem_ld_wait();
-        ETRACE(0, clock64());
+        ETRACE(cc == 0 ? 0 : 2, clock64());
 #pragma unroll
         for (int h = 0; h < 32; h += kDrain) {
           // the other half's k-th bounds this pair too (either half's K
@@ -806,7 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
               mx = fmaxf(mx, res[e + x]);
             }
           }
-          ETRACE(1 + 3 * (h / kDrain), clock64());
+
           // one compare per window; the per-column mask only when some lane
           // of the warp has a survivor in it
           uint32_t m = 0;
@@ -815,7 +826,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
             for (int e = 0; e < kDrain; ++e) m |= (res[e] >= thr ? 1u : 0u) << e;  // NaN never passes
           }
           if (__any_sync(kFull, m != 0)) {
-            ETRACE(3 + 3 * (h / kDrain), __popc(m));
+
             do {
               const int j = (__ffs(m) - 1) & (kDrain - 1);
               const float v = pick16(res, j);
@@ -826,12 +837,13 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
             *(volatile unsigned long long*)&thr_sh[half * kM + row] =
                 ((unsigned long long)tag << 32) | __float_as_uint(top.kth());
           }
-          ETRACE(2 + 3 * (h / kDrain), clock64());
+          if (h + kDrain >= 32) ETRACE(cc == 0 ? 1 : 3, clock64());
         }
       }
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      ETRACE(4, clock64());
       if (c.tile == c.ntiles - 1 && row < c.nqt) {
         // this half's partial top-k of the (query, list) pair
         const int kk = P.k;
@@ -1091,10 +1103,12 @@ static int kmax_for(int depth) { return depth <= 10 ? 10 : 32; }
 
 static bool pick_tile(int DP, int W, int C, int kmax, int* nv, int* ns, int* nacc = nullptr) {
   if (DP > kMaxDim) return false;
-  static const int shapes[2][2] = {{128, 2}, {64, 4}};  // (NV, nAcc), widest first
+  static const int shapes[3][2] = {{128, 2}, {128, 3}, {64, 4}};  // (NV, nAcc), widest first
   const char* force = getenv("IVFTQ_SCAN_NV");
+  const char* facc = getenv("IVFTQ_SCAN_ACC");
   for (const auto& sh : shapes) {
     if (force && atoi(force) != sh[0]) continue;
+    if (facc && atoi(facc) != sh[1]) continue;
     if (sh[0] * sh[1] + DP > 512) continue;  // one A buffer at least
     if (make_layout(sh[0], kNS, DP, W, C, kmax).total + 1024 > kSmemLimit) continue;
     *nv = sh[0];
@@ -1256,7 +1270,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
     std::string ep = std::string(trace_path) + ".epi";
     f = fopen(ep.c_str(), "w");
     if (f) {
-      fprintf(f, "# t ld_done w0_filter w0_drain w0_mx w1_filter w1_drain w1_mx end (rel. epi_start)\n");
+      fprintf(f, "# t ld0 win0 ld1 win1 acc_released x x end (rel. epi_start)\n");
       for (int t = 0; t < kTraceTiles; ++t) {
         const long long* e = h + 8 * kTraceTiles + t * 8;
         if (!h[t * 8 + 1]) break;
