@@ -76,6 +76,84 @@ gemm_nt_kernel(const double* __restrict__ A, const TB* __restrict__ B, int64_t M
   }
 }
 
+// 128x128 tiles, 8x8 outputs per thread (rows ty+16i, cols tx+16j): half the
+// shared-memory operand traffic per DFMA of the 64x64 kernel, which was
+// shared-memory-bound at ~42 % of the FP64 pipe. The k loop keeps the same
+// sequential FMA chain from 0.0 per output, so results are bit-identical.
+// Next K-slab prefetched into registers while the current one computes.
+constexpr int BM2 = 128, BN2 = 128, BK2 = 8, PAD2 = 132;
+
+template <typename TB, typename TC>
+__global__ void __launch_bounds__(256)
+gemm_nt_big_kernel(const double* __restrict__ A, const TB* __restrict__ B, int64_t M, int N, int K,
+                   TC* __restrict__ C) {
+  __shared__ double As[2][BK2][PAD2];
+  __shared__ double Bs[2][BK2][PAD2];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int64_t m0 = (int64_t)blockIdx.x * BM2;
+  const int n0 = blockIdx.y * BN2;
+  double acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0;
+  double ra[4], rb[4];
+  auto fetch = [&](int k0) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int i = threadIdx.x + it * 256;
+      const int r = i >> 3, kk = i & 7;
+      const int64_t gm = m0 + r;
+      const int gn = n0 + r, gk = k0 + kk;
+      ra[it] = (gm < M && gk < K) ? A[gm * K + gk] : 0.0;
+      rb[it] = (gn < N && gk < K) ? (double)B[(int64_t)gn * K + gk] : 0.0;
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int i = threadIdx.x + it * 256;
+      As[buf][i & 7][i >> 3] = ra[it];
+      Bs[buf][i & 7][i >> 3] = rb[it];
+    }
+  };
+  fetch(0);
+  stash(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < K; k0 += BK2) {
+    const bool more = k0 + BK2 < K;
+    if (more) fetch(k0 + BK2);
+    const int kmax = min(BK2, K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      double a[8], b[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = As[buf][kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) b[j] = Bs[buf][kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = __fma_rn(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      stash(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int gn = n0 + tx + 16 * j;
+      if (gn < N) C[gm * N + gn] = (TC)acc[i][j];
+    }
+  }
+}
+
 // One block owns 64 rows and sweeps every centroid tile, keeping a running
 // (max, argmax) per row; ties resolve to the lowest list id like np.argmax.
 __global__ void __launch_bounds__(256)
@@ -143,8 +221,27 @@ extern "C" int ivftq_gemm_nt(const double* A, const void* B, int b_dtype, int64_
     set_error("gemm_nt: N=%d too large", N);
     return IVFTQ_ERR_ARG;
   }
-  dim3 grid((unsigned)((M + TM - 1) / TM), (N + TN - 1) / TN);
   cudaStream_t s = (cudaStream_t)stream;
+  // measured: the 128x128 kernel wins only for tall, narrow products (the
+  // ingest rotation, 250k x 128 x 128: 490 vs 534 us); for the coarse
+  // 10k x 1024 x 128 its one-block-per-SM occupancy loses (184 vs 167 us)
+  if (M >= 65536 && N >= BN2 / 2 && N <= 256) {
+    dim3 g2((unsigned)((M + BM2 - 1) / BM2), (N + BN2 - 1) / BN2);
+    if (b_dtype == IVFTQ_F32 && c_dtype == IVFTQ_F64)
+      gemm_nt_big_kernel<float, double><<<g2, 256, 0, s>>>(A, (const float*)B, M, N, K, (double*)C);
+    else if (b_dtype == IVFTQ_F64 && c_dtype == IVFTQ_F64)
+      gemm_nt_big_kernel<double, double><<<g2, 256, 0, s>>>(A, (const double*)B, M, N, K, (double*)C);
+    else if (b_dtype == IVFTQ_F64 && c_dtype == IVFTQ_F32)
+      gemm_nt_big_kernel<double, float><<<g2, 256, 0, s>>>(A, (const double*)B, M, N, K, (float*)C);
+    else if (b_dtype == IVFTQ_F32 && c_dtype == IVFTQ_F32)
+      gemm_nt_big_kernel<float, float><<<g2, 256, 0, s>>>(A, (const float*)B, M, N, K, (float*)C);
+    else {
+      set_error("gemm_nt: bad dtypes");
+      return IVFTQ_ERR_ARG;
+    }
+    return check_launch("gemm_nt_big");
+  }
+  dim3 grid((unsigned)((M + TM - 1) / TM), (N + TN - 1) / TN);
   if (b_dtype == IVFTQ_F32 && c_dtype == IVFTQ_F64)
     gemm_nt_kernel<float, double><<<grid, 256, 0, s>>>(A, (const float*)B, M, N, K, (double*)C);
   else if (b_dtype == IVFTQ_F64 && c_dtype == IVFTQ_F64)
