@@ -243,13 +243,13 @@ def run_ours(args):
                      CoarsePartition(w.n_lists, w.d, cent), device=dev)
 
     # ---- ingest: adds/s end to end (host f32 rows -> device lists) ----------
-    chunk = 250_000
+    chunk = len(base)  # one add_batch of the whole pinned batch (sub-chunked copy/encode overlap inside)
     pinned = torch.from_numpy(base).pin_memory()
     # warm-up on a throwaway index: first-use allocations and kernel loads stay
     # out of the timed region (the timed run still grows its own store)
     warm = IvfTqIndex(cfg, design_quantizer(w.bits, w.d), generate_rotation(w.d, 42),
                       CoarsePartition(w.n_lists, w.d, cent), device=dev)
-    warm.add_batch(pinned[:chunk])
+    warm.add_batch(pinned[: min(chunk, 600_000)])
     del warm
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -260,7 +260,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ingest_s = e0.elapsed_time(e1) / 1000
     # kernel-only encode throughput on a device-resident chunk
-    xd = torch.from_numpy(base[:chunk]).to(dev)
+    xd = torch.from_numpy(base[:250_000]).to(dev)
     idx._encode_device(xd)
     torch.cuda.synchronize()
     e0.record()
@@ -433,7 +433,7 @@ def run_ours(args):
             "clocks": clk,
             "gpu_launches": int(launches),
             "ingest": {"adds_per_sec_e2e": len(base) / ingest_s,
-                       "adds_per_sec_device_encode": chunk / enc_s, "rows": len(base),
+                       "adds_per_sec_device_encode": 250_000 / enc_s, "rows": len(base),
                        "chunk": chunk},
         }
         print(json.dumps(line), flush=True)

@@ -269,9 +269,67 @@ class IvfTqIndex:
         ext = None if external_id is None else np.asarray([external_id], dtype=np.int64)
         return int(self.add_batch(np.asarray(x, dtype=np.float64)[None, :], ext)[0])
 
+    _PIPE_ROWS = 1 << 18  # host->device sub-chunk of a large host batch
+
+    def _encode_host_pipelined(self, x: torch.Tensor):
+        """Encode a large host (ideally pinned) batch in sub-chunks, copying
+        sub-chunk j+1 on a side stream while sub-chunk j encodes. Nothing is
+        appended here, so a bad row anywhere still leaves the index untouched."""
+        dev = self.device
+        n, d = x.shape
+        sub = self._PIPE_ROWS
+        if getattr(self, "_copy_stream", None) is None:
+            self._copy_stream = torch.cuda.Stream(device=dev)
+        cs = self._copy_stream
+        cur = torch.cuda.current_stream(dev)
+        bufs = [torch.empty((sub, d), dtype=x.dtype, device=dev) for _ in range(2)]
+        copied = [torch.cuda.Event() for _ in range(2)]
+        freed = [torch.cuda.Event() for _ in range(2)]
+        spans = [(s, min(n, s + sub)) for s in range(0, n, sub)]
+
+        def issue(j):
+            s, e = spans[j]
+            b = j % 2
+            with torch.cuda.stream(cs):
+                if j >= 2:
+                    cs.wait_event(freed[b])
+                bufs[b][: e - s].copy_(x[s:e], non_blocking=True)
+                copied[b].record(cs)
+
+        issue(0)
+        if len(spans) > 1:
+            issue(1)
+        parts = []
+        keep_xn = self._raw is not None
+        for j, (s, e) in enumerate(spans):
+            b = j % 2
+            cur.wait_event(copied[b])
+            try:
+                words, lids, nrm, xn = self._encode_device(bufs[b][: e - s])
+            except ValueError as err:
+                msg = str(err)
+                if "row at index" in msg:  # report the index within the whole batch
+                    i = int(msg.rsplit(" ", 1)[1])
+                    raise ValueError(f"zero-norm input row at index {s + i}") from None
+                raise
+            freed[b].record(cur)
+            if j + 2 < len(spans):
+                issue(j + 2)
+            parts.append((words, lids, nrm, xn if keep_xn else None))
+        words = torch.cat([p[0] for p in parts])
+        lids = torch.cat([p[1] for p in parts])
+        nrm = torch.cat([p[2] for p in parts])
+        xn = torch.cat([p[3] for p in parts]) if keep_xn else None
+        return words, lids, nrm, xn
+
     def add_batch(self, x, external_ids: np.ndarray | None = None) -> np.ndarray:
         """Encode and append rows; returns internal ids (index.py:286-310)."""
-        words, lids, nrm, xn = self._encode_device(x)
+        if (isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.dim() == 2
+                and x.shape[1] == self.config.dim and x.shape[0] > 2 * self._PIPE_ROWS
+                and x.dtype in (torch.float32, torch.float64)):
+            words, lids, nrm, xn = self._encode_host_pipelined(x)
+        else:
+            words, lids, nrm, xn = self._encode_device(x)
         n = words.shape[0]
         if external_ids is None:
             external_ids = np.arange(self._count, self._count + n, dtype=np.int64)

@@ -512,3 +512,29 @@ def test_assign_tc_identical_to_f64(n, L, d):
     np.testing.assert_array_equal(out_tc.cpu().numpy(), out_64.cpu().numpy())
     np.testing.assert_array_equal(out_tc.cpu().numpy(),
                                   np.argmax(x @ c.astype(np.float64).T, axis=1))
+
+
+def test_pipelined_host_ingest_equals_plain(golden):
+    """Large host batches are encoded in sub-chunks while the next one copies;
+    the stored fields must equal a plain add, and a zero row anywhere must
+    still raise with its batch-wide index before anything is appended."""
+    import torch
+
+    g = golden("d128_b4_L64")
+    x = g["x"].astype(np.float32)
+    a = index_from_golden(g)
+    a.add_batch(x)
+    b = index_from_golden(g)
+    b._PIPE_ROWS = 256  # force several sub-chunks
+    b.add_batch(torch.from_numpy(x).pin_memory())
+    np.testing.assert_array_equal(a.list_ids, b.list_ids)
+    np.testing.assert_array_equal(a.bins, b.bins)
+    np.testing.assert_array_equal(a.signs, b.signs)
+    np.testing.assert_array_equal(a.norms.view(np.uint16), b.norms.view(np.uint16))
+    c = index_from_golden(g)
+    c._PIPE_ROWS = 256
+    bad = x.copy()
+    bad[700] = 0
+    with pytest.raises(ValueError, match="row at index 700"):
+        c.add_batch(torch.from_numpy(bad))
+    assert c.count == 0
