@@ -547,10 +547,18 @@ class IvfTqIndex:
             if int(bad.item()) < nq:
                 raise ValueError("zero-norm query")
             return ids[:nq], scores[:nq]
-        b = int(bad.item())
-        if b < nq:
+        # one synchronisation: results and the bad-row flag land in pinned
+        # host buffers (torch's caching host allocator) with async copies
+        ih = torch.empty((nq, ids.shape[1]), dtype=ids.dtype, pin_memory=True)
+        sh = torch.empty((nq, scores.shape[1]), dtype=scores.dtype, pin_memory=True)
+        bh = torch.empty(1, dtype=bad.dtype, pin_memory=True)
+        ih.copy_(ids[:nq], non_blocking=True)
+        sh.copy_(scores[:nq], non_blocking=True)
+        bh.copy_(bad, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        if int(bh[0]) < nq:
             raise ValueError("zero-norm query")
-        return ids[:nq].cpu().numpy(), scores[:nq].cpu().numpy()
+        return ih.numpy(), sh.numpy()
 
     def _search_flat_batch(self, queries, k, return_device=False):
         """Exhaustive flat scan, score = <Pi q, rho_hat> (index.py:485-500)."""
