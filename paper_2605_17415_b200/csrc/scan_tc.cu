@@ -45,7 +45,8 @@
 namespace ivftq {
 
 void launch_merge(const double* part_s, const int32_t* part_id, int64_t nq, int n_in, int K,
-                  int64_t* ids_out, double* s_out, cudaStream_t s);
+                  int64_t* ids_out, double* s_out, cudaStream_t s,
+                  const int32_t* counts = nullptr);
 int merge_smem_opt_in(int K);
 
 namespace tc {
@@ -153,13 +154,15 @@ struct Params {
   const int2* items;       // (list, query tile)
   const int32_t* n_items;  // device scalar
   int32_t* counter;        // work counter (zeroed per launch)
-  double* part_s;          // [nq*n_p*k]
+  double* part_s;          // [nq][2*n_p*k] per-query candidate buffer
   int32_t* part_id;
+  int32_t* qcnt;           // [nq] candidates appended per query
   long long* thr_key;      // [nq] order-preserving key of a lower bound on the k-th score
   long long* trace;        // debug timeline of CTA 0 (IVFTQ_TRACE), else null
   const uint32_t* q_hi;    // [nq][DP/2] rotated query rows, fp16 hi halves (x 2^14), packed pairs
   const uint32_t* q_lo;    // [nq][DP/2] matching lo halves
   int n_p, k, d, DP, NV, NS;
+  int qcap;         // candidate buffer capacity per query (2*n_p*k)
   int nAcc;         // TMEM accumulator ring depth (<= kAccMax)
   int nA;           // A-operand buffers in TMEM (2 when they fit: next item's
                     // queries are written while the current item's MMAs run)
@@ -485,16 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const int size = P.st.list_size[l];
       const int64_t off = P.st.list_offset[l];
       const int ntiles = (size + NV - 1) / NV;
-      if (ntiles == 0) {  // empty list: every probing query gets -inf padding
-        for (int r = lane; r < nqt; r += 32) {
-          const int64_t ob = (int64_t)P.pair_idx[pbase + r] * 2 * P.k;
-          for (int p = 0; p < 2 * P.k; ++p) {
-            P.part_s[ob + p] = -INFINITY;
-            P.part_id[ob + p] = INT_MAX;
-          }
-        }
-        continue;
-      }
+      if (ntiles == 0) continue;  // empty list: contributes no candidates
       int prow[kM / 32];
       double pcs[kM / 32];
       long long kq[kM / 32];
@@ -845,35 +839,33 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       if (lane == 0) mbar_arrive(&acc_empty[ab]);
       ETRACE(4, clock64());
       if (c.tile == c.ntiles - 1 && row < c.nqt) {
-        // this half's partial top-k of the (query, list) pair
+        // Append this half's candidates of the (query, list) pair to the
+        // query's buffer -- only those at or above the query's current global
+        // bound: thr_key only rises and lower-bounds the final k-th score, so
+        // anything below it can never be returned (ties at the bound are kept).
+        const int q = pi / P.n_p;
+        const double bound = dkey_inv(*(volatile const long long*)&P.thr_key[q]);
         const int kk = P.k;
-        const int64_t o = ((int64_t)pi * 2 + half) * kk;
         double sv[KMAX];
-        int iv[KMAX];
+        int m = 0;
 #pragma unroll
         for (int p = 0; p < KMAX; ++p) {
-          const bool have = top.k[p] != 0;
-          sv[p] = have ? cs + (double)key_score(top.k[p]) : -INFINITY;
-          iv[p] = have ? key_id(top.k[p]) : INT_MAX;
+          sv[p] = top.k[p] ? cs + (double)key_score(top.k[p]) : -INFINITY;
+          if (p < kk && top.k[p] && sv[p] >= bound) m = p + 1;  // sorted: a prefix
         }
-        if (kk == KMAX) {  // 16-byte / 8-byte vector stores (o is even: KMAX is)
-#pragma unroll
-          for (int p = 0; p < KMAX; p += 2) {
-            *(double2*)(P.part_s + o + p) = make_double2(sv[p], sv[p + 1]);
-            *(int2*)(P.part_id + o + p) = make_int2(iv[p], iv[p + 1]);
-          }
-        } else {
+        if (m) {
+          const int64_t o = (int64_t)q * P.qcap + atomicAdd(&P.qcnt[q], m);
 #pragma unroll
           for (int p = 0; p < KMAX; ++p)
-            if (p < kk) {
+            if (p < m) {
               P.part_s[o + p] = sv[p];
-              P.part_id[o + p] = iv[p];
+              P.part_id[o + p] = key_id(top.k[p]);
             }
         }
         // KMAX >= k candidates of this query score >= this K-th: a global lower
         // bound on its final k-th that prunes its other lists
         if (top.k[KMAX - 1] != 0)
-          atomicMax(&P.thr_key[pi / P.n_p], dkey(cs + (double)key_score(top.k[KMAX - 1])));
+          atomicMax(&P.thr_key[q], dkey(sv[KMAX - 1]));
       }
       __syncwarp();
       ETRACE(7, clock64());
@@ -1049,6 +1041,7 @@ struct TcScratch {
   int2* items;
   double* part_s;
   int32_t* part_id;
+  int32_t* qcnt;
   char* zero_end;
   int T;
   size_t bytes;
@@ -1074,6 +1067,7 @@ static TcScratch carve_tc(void* base, int64_t nq, int n_p, int L, int k, int dim
   S.G = (int32_t*)take(4 * (size_t)S.T);
   S.fill = (int32_t*)take(4 * (size_t)S.T);
   S.counter = (int32_t*)take(16);
+  S.qcnt = (int32_t*)take(4 * (size_t)nq);
   S.zero_end = b ? b + off : nullptr;
   S.pstart2 = (int32_t*)take(4 * ((size_t)L * kRC + 1));
   S.pstart = (int32_t*)take(4 * (size_t)(L + 1));
@@ -1202,6 +1196,8 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   P.counter = S.counter;
   P.part_s = S.part_s;
   P.part_id = S.part_id;
+  P.qcnt = S.qcnt;
+  P.qcap = n_p * 2 * depth;
   P.thr_key = S.thr_key;
   P.q_hi = S.q_hi;
   P.q_lo = S.q_lo;
@@ -1283,6 +1279,6 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
     cudaFree(trace);
   }
   if (int e = merge_smem_opt_in(depth)) return e;
-  launch_merge(S.part_s, S.part_id, nq, n_p * 2 * depth, depth, ids_out, scores_out, s);
+  launch_merge(S.part_s, S.part_id, nq, n_p * 2 * depth, depth, ids_out, scores_out, s, S.qcnt);
   return check_launch("merge");
 }

@@ -422,12 +422,13 @@ template <int QS>
 __global__ void __launch_bounds__(256)
 merge_warp_kernel(const double* __restrict__ part_s, const int32_t* __restrict__ part_id,
                   int64_t nq, int n_in, int K, int64_t* __restrict__ ids_out,
-                  double* __restrict__ s_out) {
+                  double* __restrict__ s_out, const int32_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= nq) return;
   const double* ps = part_s + q * n_in;
   const int32_t* pi = part_id + q * n_in;
+  if (counts) n_in = min(n_in, counts[q]);  // compact per-query buffer
   long long qk[QS];
   int qi[QS];
 #pragma unroll
@@ -638,13 +639,14 @@ int merge_smem_opt_in(int K) {
   return smem_opt_in((const void*)merge_kernel, BlockTopK::bytes(topk_cap(K, 128)));
 }
 void launch_merge(const double* part_s, const int32_t* part_id, int64_t nq, int n_in, int K,
-                  int64_t* ids_out, double* s_out, cudaStream_t s) {
+                  int64_t* ids_out, double* s_out, cudaStream_t s,
+                  const int32_t* counts = nullptr) {
   const unsigned wb = (unsigned)((nq + 7) / 8);
   if (K <= 32)
-    merge_warp_kernel<1><<<wb, 256, 0, s>>>(part_s, part_id, nq, n_in, K, ids_out, s_out);
+    merge_warp_kernel<1><<<wb, 256, 0, s>>>(part_s, part_id, nq, n_in, K, ids_out, s_out, counts);
   else if (K <= 64)
-    merge_warp_kernel<2><<<wb, 256, 0, s>>>(part_s, part_id, nq, n_in, K, ids_out, s_out);
-  else
+    merge_warp_kernel<2><<<wb, 256, 0, s>>>(part_s, part_id, nq, n_in, K, ids_out, s_out, counts);
+  else  // deep rerank lists (LUT path only; the tensor-core scan caps depth at 32)
     merge_kernel<<<(unsigned)nq, 128, BlockTopK::bytes(topk_cap(K, 128)), s>>>(
         part_s, part_id, n_in, K, ids_out, s_out);
 }
