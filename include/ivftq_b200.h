@@ -100,7 +100,8 @@ int ivftq_assign_tc(const double* xn, const float* centroids, int64_t n, int n_l
                     void* stream);
 /* Coarse-scoring path selection (results are identical in every mode):
  * 0 = default: assignment on tensor cores with the f64 guard band (dim <= 256),
- *     probes on the f64 GEMM + exact select;
+ *     probes on tensor cores when n_lists >= 32 * n_p, else the f64 GEMM +
+ *     exact select (the faster of the two on B200);
  * 1 = f64 CUDA-core GEMMs only (parity reference);
  * 2 = tensor cores for probes as well (also IVFTQ_PROBE_TC=1). */
 int ivftq_set_coarse_mode(int mode);

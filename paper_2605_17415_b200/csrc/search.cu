@@ -572,6 +572,8 @@ int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, 
              int n_p, int32_t* probe_out, double* coarse_out, void* scratch,
              size_t scratch_bytes, cudaStream_t s);
 extern "C" size_t ivftq_probe_tc_scratch_bytes(int64_t nq, int n_lists, int dim);
+extern "C" int ivftq_coarse_tc_supported(int dim, int n_lists);
+static bool probe_tc_auto() { return ivftq_coarse_tc_supported(128, 1) != 0; }  // mode != 1
 static bool probe_tc_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -603,12 +605,14 @@ extern "C" int ivftq_probe(const double* qn, const float* centroids, int64_t nq,
     return IVFTQ_ERR_ARG;
   }
   if (nq == 0) return 0;
-  // Probes take the f64 GEMM + exact select by default: every selected probe
-  // needs its exact f64 coarse score, and re-scoring ~n_p gathered centroid
-  // rows per query (no reuse across queries) measured slower than the dense
-  // f64 GEMM at C2 (325 us vs 167 us). IVFTQ_PROBE_TC=1 selects the tcgen05
-  // path (identical results; tests exercise both).
-  if (probe_tc_enabled()) {
+  // Path choice (results identical): the tensor-core path pays a dense
+  // tcgen05 GEMM plus an exact f64 re-score of ~n_p gathered centroid rows
+  // per query; the f64 path a dense DFMA GEMM. Measured on B200
+  // (scripts/probe_mode_bench.py, nq = 10k): L=1024 n_p=64: f64 0.24 ms vs
+  // 0.47; L=4096 n_p=32: 0.72 vs 0.52; n_p=128: 0.86 vs 0.88; d=200 n_p=64:
+  // 1.21 vs 0.91 -- so tensor cores when L >= 32 n_p (mode 0), always
+  // (mode 2 / IVFTQ_PROBE_TC=1), never (mode 1).
+  if (probe_tc_enabled() || (probe_tc_auto() && n_lists >= 32 * n_p)) {
     const int e = probe_tc(qn, centroids, nq, n_lists, dim, n_p, probe_out, coarse_out, scratch,
                            scratch_bytes, (cudaStream_t)stream);
     if (e != IVFTQ_ERR_UNSUPPORTED) return e;
