@@ -10,9 +10,12 @@ from paper_2605_17415_b200 import CoarsePartition, design_quantizer, generate_ro
 from paper_2605_17415_b200.index import IndexConfig, IvfTqIndex
 from paper_2605_17415_b200.workloads import mixture
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-nq, d, L, n_p = 10_000, 128, 1024, int(sys.argv[2]) if len(sys.argv) > 2 else 64
-x, means = mixture(n, d, 1000, 0.3, 1)
-q, _ = mixture(nq, d, 1000, 0.3, 2, means=means)
+n_p = int(sys.argv[2]) if len(sys.argv) > 2 else 64
+d = int(sys.argv[3]) if len(sys.argv) > 3 else 128
+L = int(sys.argv[4]) if len(sys.argv) > 4 else 1024
+nq = 10_000
+x, means = mixture(n, d, L, 0.3, 1)
+q, _ = mixture(nq, d, L, 0.3, 2, means=means)
 rng = np.random.default_rng(0)
 cent = x[rng.choice(n, L, replace=False)].astype(np.float64)
 cent = (cent / np.linalg.norm(cent, axis=1)[:, None]).astype(np.float32)
