@@ -7,26 +7,29 @@
 //
 //   * probes are regrouped by list on the device (count / scan / scatter);
 //     a work item is (list l, tile of <=128 queries probing l);
-//   * persistent CTAs, one per SM, run a four-role pipeline over the stream of
-//     NV-vector tiles of their items, handing off through mbarrier rings:
-//       - producer warp: pulls items from an atomic counter, writes the tile's
-//         control record + query rows into a stage slot, and one lane issues a
-//         1-D TMA bulk copy of the tile's packed codes, norms and ids (the
-//         32-slot interleaved list layout makes a tile one contiguous span);
-//       - 4 decoder warps: on an item's first tile build the A operand (the
-//         item's rotated queries, fp16 hi/lo) and, per tile, decode codes
-//         through a 2^(b+1)-entry level table into the B operand (UMMA K-major
-//         canonical layout, fp16 hi/lo), double-buffered;
-//       - MMA warp: one thread issues tcgen05.mma kind::f16 (3 products per
-//         K step, see below) into a double-buffered TMEM accumulator
-//         D[query][vector] and commits to the ring barriers;
+//   * persistent CTAs, one per SM (23 warps), run a pipeline over the stream
+//     of NV-vector tiles (NV = 128, or 64 for wide d) of their items, handing
+//     off through mbarrier rings:
+//       - scheduler warp: pulls items from an atomic counter and prepares an
+//         item record (list span, query rows, coarse scores, initial bounds)
+//         up to two items ahead, prefetching the rows' A operands into L2;
+//       - producer warp: per tile, query rows + fresh pruning bounds into a
+//         stage slot, then one lane issues 1-D TMA bulk copies of the tile's
+//         packed codes, norms and ids (the 32-slot interleaved list layout
+//         makes each a contiguous span);
+//       - 4 A-builder warps (one per TMEM lane quadrant): the item's rotated
+//         queries as fp16 hi/lo into TMEM (the MMA A operand), one item ahead;
+//       - 8 decoder warps: codes -> B operand (UMMA K-major canonical layout,
+//         fp16 hi/lo) through a 2^(b+1)-entry level table, double-buffered;
+//       - MMA warp: elected lane issues tcgen05.mma kind::f16 (3 products per
+//         K step, see below) into a TMEM accumulator ring D[query][vector];
 //       - 8 epilogue warps: warp w reads TMEM lanes 32*(w%4).. (one query per
-//         thread) over half of the tile's columns, filters candidates against
-//         the query's running k-th score, appends survivors to a per-thread
-//         shared buffer and drains it into a register top-K (the drain loop
-//         runs to the warp's max survivor count, so inserts stay convergent);
-//         at an item's last tile the two halves merge and (query, list)
-//         winners go to a buffer that a second kernel merges per query.
+//         thread) over half of the tile's columns, filters 16-column windows
+//         against the pair's running k-th / the other half's / the query's
+//         global bound, and inserts survivors into a branch-free register
+//         top-K of 64-bit (score, ~id) keys; at an item's last tile each half
+//         appends its entries above the global bound to the query's buffer,
+//         which a second kernel merges per query.
 //
 // Numerics: f32 values are split into fp16 hi + lo with power-of-two scaling
 // (T by 2^eT, q by 2^14) and D = Qhi.Thi + Qlo.Thi + Qhi.Tlo accumulated in
@@ -627,11 +630,38 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       ++t;
     }
   } else if (warp < kEpiWarp0) {
-    // ================= decoders (+ A operand builders) =========================
-    const int dt_ = tid - 32 * kDecWarp0;  // 0..127
+    // ================= decoders ==============================================
+    const int dt_ = tid - 32 * kDecWarp0;  // 0..255
     constexpr int kDecThreads = 32 * kDecWarps;
     const int NG = (DP + G - 1) / G;
-    uint32_t t = 0, u = 0;
+    // Tile record for the MMA issuer and the epilogue (ctrl, query rows +
+    // bounds, scaled norms, ids), copied out of the stage slot so the slot
+    // returns to the producer as soon as decoding is done.
+    auto publish_meta = [&](uint32_t t, const Ctrl& c, const unsigned char* sp) {
+      const int ms = t & (kMeta - 1);
+      if (t >= (uint32_t)kMeta) sm100::mbar_wait_sleep(&meta_empty[ms], ((t / kMeta) - 1) & 1);
+      DTRACE(5);
+      unsigned char* mp = meta(ms);
+      if (dt_ == 0) *(Ctrl*)mp = c;
+      if (c.list >= 0) {
+        const int* qsrc = (const int*)(sp + Lo.st_qrow);
+        const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
+        const int* idsrc = (const int*)(sp + Lo.st_ids);
+        int* qdst = (int*)(mp + Lo.m_qrow);
+        float* nsc = (float*)(mp + Lo.m_nsc);
+        int* idd = (int*)(mp + Lo.m_ids);
+        for (int i = dt_; i < 2 * kM; i += kDecThreads) qdst[i] = qsrc[i];
+        for (int v = dt_; v < NV; v += kDecThreads) {
+          const bool ok = v < c.valid;
+          nsc[v] = ok ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
+                      : __int_as_float(0x7fc00000);
+          idd[v] = ok ? idsrc[v] : INT_MAX;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&meta_full[ms]);
+    };
+    uint32_t t = 0;
     for (;;) {
       const int s = t % NS;
       sm100::mbar_wait_sleep(&st_full[s], (t / NS) & 1);
@@ -642,32 +672,8 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       DTRACE(0);
       if (t >= 2) sm100::mbar_wait_sleep(&op_empty[ob], ((t >> 1) - 1) & 1);
       DTRACE(1);
-      if (c.list < 0) {
-        // ---- tile record for the MMA issuer and the epilogue (copied out so the
-      //      stage slot returns to the producer as soon as decoding is done) ------
-      const int ms = t & (kMeta - 1);
-      if (t >= (uint32_t)kMeta) sm100::mbar_wait_sleep(&meta_empty[ms], ((t / kMeta) - 1) & 1);
-      {
-        unsigned char* mp = meta(ms);
-        if (dt_ == 0) *(Ctrl*)mp = c;
-        if (c.list >= 0) {
-          const int* qsrc = (const int*)(sp + Lo.st_qrow);
-          const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
-          const int* idsrc = (const int*)(sp + Lo.st_ids);
-          int* qdst = (int*)(mp + Lo.m_qrow);
-          float* nsc = (float*)(mp + Lo.m_nsc);
-          int* idd = (int*)(mp + Lo.m_ids);
-          for (int i = dt_; i < 2 * kM; i += kDecThreads) qdst[i] = qsrc[i];
-          for (int v = dt_; v < NV; v += kDecThreads) {
-            const bool ok = v < c.valid;
-            nsc[v] = ok ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
-                        : __int_as_float(0x7fc00000);
-            idd[v] = ok ? idsrc[v] : INT_MAX;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&meta_full[ms]);
-      }
+      if (c.list < 0) {  // stop record: forward it to the MMA issuer and the epilogue
+        publish_meta(t, c, sp);
         __syncwarp();
         if (lane == 0) mbar_arrive(&op_full[ob]);
         break;
@@ -711,32 +717,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       }
       sm100::fence_proxy_async_smem();
       DTRACE(4);
-      // ---- tile record for the MMA issuer and the epilogue (copied out so the
-      //      stage slot returns to the producer as soon as decoding is done) ------
-      const int ms = t & (kMeta - 1);
-      if (t >= (uint32_t)kMeta) sm100::mbar_wait_sleep(&meta_empty[ms], ((t / kMeta) - 1) & 1);
-      DTRACE(5);
-      {
-        unsigned char* mp = meta(ms);
-        if (dt_ == 0) *(Ctrl*)mp = c;
-        if (c.list >= 0) {
-          const int* qsrc = (const int*)(sp + Lo.st_qrow);
-          const uint16_t* nrm = (const uint16_t*)(sp + Lo.st_norms);
-          const int* idsrc = (const int*)(sp + Lo.st_ids);
-          int* qdst = (int*)(mp + Lo.m_qrow);
-          float* nsc = (float*)(mp + Lo.m_nsc);
-          int* idd = (int*)(mp + Lo.m_ids);
-          for (int i = dt_; i < 2 * kM; i += kDecThreads) qdst[i] = qsrc[i];
-          for (int v = dt_; v < NV; v += kDecThreads) {
-            const bool ok = v < c.valid;
-            nsc[v] = ok ? __half2float(__ushort_as_half(nrm[v])) * P.inv_scale
-                        : __int_as_float(0x7fc00000);
-            idd[v] = ok ? idsrc[v] : INT_MAX;
-          }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&meta_full[ms]);
-      }
+      publish_meta(t, c, sp);
       __syncwarp();
       if (warp == kDecWarp0) TRACE(2);
       if (lane == 0) {
