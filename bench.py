@@ -228,16 +228,11 @@ def run_ours(args):
     from paper_2605_17415_b200.quantizer import design_quantizer
     from paper_2605_17415_b200.rotation import generate_rotation
 
+    from paper_2605_17415_b200.replicas import job_throughput, max_over_ranks, share_centroids
+
     L = _lib.lib()
     w, base, xn, queries, nq, n_p = setup(args, rank)
-    if rank == 0:
-        cent = train_centroids(w, xn)
-        ct = torch.from_numpy(cent).to(dev)
-    else:
-        ct = torch.empty((w.n_lists, w.d), dtype=torch.float32, device=dev)
-    if world > 1:
-        dist.broadcast(ct, 0)
-    cent = ct.cpu().numpy()
+    cent = share_centroids(train_centroids(w, xn) if rank == 0 else None, (w.n_lists, w.d), dev)
     cfg = IndexConfig(dim=w.d, bits=w.bits, n_lists=w.n_lists)
     idx = IvfTqIndex(cfg, design_quantizer(w.bits, w.d), generate_rotation(w.d, 42),
                      CoarsePartition(w.n_lists, w.d, cent), device=dev)
@@ -315,12 +310,8 @@ def run_ours(args):
         launches += L.ivftq_launch_count() - c0
         times.append(e0.elapsed_time(e1))
     clk = clocks.stop()
-    ms = float(np.mean(times))
-    tmax = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-    ms_max = float(tmax.item())
-    value = nq * world / (ms_max / 1000)
+    ms_max = max_over_ranks(float(np.mean(times)), dev)
+    value = job_throughput(nq, ms_max)
     recall = recall_at_k(ids.cpu().numpy(), truth, 10)
 
     # ---- e2e through the public API with host buffers -----------------------
@@ -335,11 +326,7 @@ def run_ours(args):
         e1.record()
         torch.cuda.synchronize()
         e2e_t.append(e0.elapsed_time(e1))
-    e2e_ms = float(np.mean(e2e_t))
-    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_val = nq * world / (float(te.item()) / 1000)
+    e2e_val = job_throughput(nq, max_over_ranks(float(np.mean(e2e_t)), dev))
 
     # ---- roofline of the dominant kernel (list scan) ------------------------
     import ctypes as C
