@@ -979,6 +979,53 @@ __global__ void q16_kernel(const float* __restrict__ qrot, int64_t nq, int d, in
   lo[i] = l0 | (l1 << 16);
 }
 
+// Seed each query's global pruning bound before the scan: score the first
+// (up to) 32 slots of the query's nearest probed list exactly as the LUT scan
+// would (f32 q_rot * f32 T, sequential, times the f32 norm, plus the f64
+// coarse score) and take the k-th best. Those are k real candidates, so the
+// query's final k-th score is at least their k-th; the margin covers the
+// difference between this f32 arithmetic and the tensor-core scan's
+// (|res| <= ~1 with ~2^-22 relative error each way). One warp per query.
+__global__ void __launch_bounds__(256)
+seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
+                  const double* __restrict__ coarse, const float* __restrict__ qrot,
+                  const double* __restrict__ levels, int64_t nq, int n_p, int k,
+                  long long* __restrict__ key) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (q >= nq) return;
+  const int l0 = probe[q * n_p];
+  const int m = min(st.list_size[l0], 32);
+  double sc = -INFINITY;
+  if (lane < m) {
+    const int64_t slot = st.list_offset[l0] + lane;
+    const int fb = st.field_bits, fpw = st.fields_per_word, W = st.words_per_vec;
+    const uint32_t mask = (1u << fb) - 1u;
+    const uint32_t* cw = st.codes + (slot >> 5) * W * 32 + (slot & 31);
+    const float* qr = qrot + q * st.dim;
+    float acc = 0.f;
+    for (int w = 0, j = 0; w < W; ++w) {
+      const uint32_t word = cw[w * 32];
+      for (int f = 0; f < fpw && j < st.dim; ++f, ++j)
+        acc = __fadd_rn(acc, __fmul_rn(qr[j], (float)levels[(word >> (f * fb)) & mask]));
+    }
+    const float nrm = __half2float(__ushort_as_half(st.norms[slot]));
+    sc = coarse[q * n_p] + (double)__fmul_rn(nrm, acc);
+  }
+  // k-th best of the lane scores: the largest value with at least k values
+  // >= it (lanes without a slot hold -inf and never qualify)
+  int ge = 0;
+  for (int o = 0; o < 32; ++o) ge += __shfl_sync(kFull, sc, o) >= sc;
+  double kth = (ge >= k && sc > -INFINITY) ? sc : -INFINITY;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) kth = fmax(kth, __shfl_xor_sync(kFull, kth, o));
+  if (lane == 0) {
+    double b = -INFINITY;
+    if (m >= k && kth > -INFINITY) b = kth - (1e-5 + 1e-5 * fabs(kth));
+    key[q] = dkey(b);
+  }
+}
+
 __global__ void thr_init_kernel(long long* __restrict__ key, int64_t n) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) key[i] = dkey(-INFINITY);
@@ -1143,7 +1190,14 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   int64_t np = nq * n_p;
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(S.cnt2, 0, S.zero_end - (char*)S.cnt2, s));
   unsigned gp = (unsigned)((np + 255) / 256);
-  thr_init_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(S.thr_key, nq);
+  // global pruning bounds: seeded from each query's nearest list (exactness
+  // preserved by a margin), unless disabled for measurement
+  if (getenv("IVFTQ_NO_SEED")) {
+    thr_init_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(S.thr_key, nq);
+  } else {
+    seed_bound_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, s>>>(*st, probe, coarse, qrot, levels,
+                                                               nq, n_p, depth, S.thr_key);
+  }
   if (int e = check_launch("thr_init")) return e;
   pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.cnt2);
   if (int e = check_launch("pair_count")) return e;
