@@ -980,43 +980,66 @@ __global__ void q16_kernel(const float* __restrict__ qrot, int64_t nq, int d, in
 }
 
 // Seed each query's global pruning bound before the scan: score the first
-// (up to) 32 slots of the query's nearest probed list exactly as the LUT scan
+// (up to) 32*P slots of the query's nearest probed list exactly as the LUT scan
 // would (f32 q_rot * f32 T, sequential, times the f32 norm, plus the f64
 // coarse score) and take the k-th best. Those are k real candidates, so the
 // query's final k-th score is at least their k-th; the margin covers the
 // difference between this f32 arithmetic and the tensor-core scan's
 // (|res| <= ~1 with ~2^-22 relative error each way). One warp per query.
+template <int P>
 __global__ void __launch_bounds__(256)
 seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
                   const double* __restrict__ coarse, const float* __restrict__ qrot,
                   const double* __restrict__ levels, int64_t nq, int n_p, int k,
                   long long* __restrict__ key) {
-  const int lane = threadIdx.x & 31;
-  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  __shared__ float t32[256];          // f32 level table (2^(bits+1) <= 256 fields)
+  __shared__ float qs_all[8][kMaxDim];  // each warp's rotated query row
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fb = st.field_bits, fpw = st.fields_per_word, W = st.words_per_vec;
+  for (int c = threadIdx.x; c < (1 << fb); c += blockDim.x) t32[c] = (float)levels[c];
+  const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+  float* qr = qs_all[warp];
+  if (q < nq)
+    for (int j = lane; j < st.dim; j += 32) qr[j] = qrot[q * st.dim + j];
+  __syncthreads();
   if (q >= nq) return;
   const int l0 = probe[q * n_p];
-  const int m = min(st.list_size[l0], 32);
-  double sc = -INFINITY;
-  if (lane < m) {
-    const int64_t slot = st.list_offset[l0] + lane;
-    const int fb = st.field_bits, fpw = st.fields_per_word, W = st.words_per_vec;
-    const uint32_t mask = (1u << fb) - 1u;
-    const uint32_t* cw = st.codes + (slot >> 5) * W * 32 + (slot & 31);
-    const float* qr = qrot + q * st.dim;
-    float acc = 0.f;
-    for (int w = 0, j = 0; w < W; ++w) {
-      const uint32_t word = cw[w * 32];
-      for (int f = 0; f < fpw && j < st.dim; ++f, ++j)
-        acc = __fadd_rn(acc, __fmul_rn(qr[j], (float)levels[(word >> (f * fb)) & mask]));
+  const int m = min(st.list_size[l0], 32 * P);
+  const uint32_t mask = (1u << fb) - 1u;
+  const double cs = coarse[q * n_p];
+  double sc[P];
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    sc[p] = -INFINITY;
+    const int i = p * 32 + lane;
+    if (i < m) {
+      const int64_t slot = st.list_offset[l0] + i;
+      const uint32_t* cw = st.codes + (slot >> 5) * W * 32 + (slot & 31);
+      float acc = 0.f;
+      for (int w0 = 0, j = 0; w0 < W; w0 += 8) {  // 8 words in flight per batch
+        uint32_t wd[8];
+#pragma unroll
+        for (int x = 0; x < 8; ++x) wd[x] = w0 + x < W ? cw[(w0 + x) * 32] : 0u;
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+          for (int f = 0; f < fpw && j < st.dim && w0 + x < W; ++f, ++j)
+            acc = __fadd_rn(acc, __fmul_rn(qr[j], t32[(wd[x] >> (f * fb)) & mask]));
+      }
+      const float nrm = __half2float(__ushort_as_half(st.norms[slot]));
+      sc[p] = cs + (double)__fmul_rn(nrm, acc);
     }
-    const float nrm = __half2float(__ushort_as_half(st.norms[slot]));
-    sc = coarse[q * n_p] + (double)__fmul_rn(nrm, acc);
   }
-  // k-th best of the lane scores: the largest value with at least k values
-  // >= it (lanes without a slot hold -inf and never qualify)
-  int ge = 0;
-  for (int o = 0; o < 32; ++o) ge += __shfl_sync(kFull, sc, o) >= sc;
-  double kth = (ge >= k && sc > -INFINITY) ? sc : -INFINITY;
+  // k-th best: the largest value with at least k values >= it (slots past
+  // the list hold -inf and never qualify)
+  double kth = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < P; ++p) {
+    int ge = 0;
+    for (int o = 0; o < 32; ++o)
+#pragma unroll
+      for (int r = 0; r < P; ++r) ge += __shfl_sync(kFull, sc[r], o) >= sc[p];
+    if (ge >= k && sc[p] > -INFINITY) kth = fmax(kth, sc[p]);
+  }
 #pragma unroll
   for (int o = 16; o; o >>= 1) kth = fmax(kth, __shfl_xor_sync(kFull, kth, o));
   if (lane == 0) {
@@ -1195,8 +1218,18 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   if (getenv("IVFTQ_NO_SEED")) {
     thr_init_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(S.thr_key, nq);
   } else {
-    seed_bound_kernel<<<(unsigned)((nq + 7) / 8), 256, 0, s>>>(*st, probe, coarse, qrot, levels,
-                                                               nq, n_p, depth, S.thr_key);
+    const char* sp_env = getenv("IVFTQ_SEED_P");
+    const int sp = sp_env ? atoi(sp_env) : 1;
+    const unsigned sb = (unsigned)((nq + 7) / 8);
+    if (sp >= 4)
+      seed_bound_kernel<4><<<sb, 256, 0, s>>>(*st, probe, coarse, qrot, levels, nq, n_p, depth,
+                                              S.thr_key);
+    else if (sp == 2)
+      seed_bound_kernel<2><<<sb, 256, 0, s>>>(*st, probe, coarse, qrot, levels, nq, n_p, depth,
+                                              S.thr_key);
+    else
+      seed_bound_kernel<1><<<sb, 256, 0, s>>>(*st, probe, coarse, qrot, levels, nq, n_p, depth,
+                                              S.thr_key);
   }
   if (int e = check_launch("thr_init")) return e;
   pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.cnt2);
