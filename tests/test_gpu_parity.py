@@ -538,3 +538,28 @@ def test_pipelined_host_ingest_equals_plain(golden):
     with pytest.raises(ValueError, match="row at index 700"):
         c.add_batch(torch.from_numpy(bad))
     assert c.count == 0
+
+
+@pytest.mark.parametrize("k,n_p,nq", [(50, 64, 100), (33, 8, 100), (10, 64, 100), (1, 1, 100),
+                                      (10, 4, 0), (10, 16, 1), (5, 200, 70)])
+def test_search_shapes_against_oracle(golden, k, n_p, nq):
+    """Depths past the tensor-core range (k > 32), every list probed, empty and
+    single-query batches, n_p clamped above L -- all against the oracle."""
+    import warnings as w_
+
+    from oracle import ivftq_oracle as orc
+
+    g = golden("d128_b4_L64")
+    idx = index_from_golden(g)
+    idx.add_batch(g["x"])
+    o = orc.OracleIndex(g["centroids"], g["R"], g["boundaries"], g["qcent"], g["half"])
+    o.add_batch(g["x"])
+    rng = np.random.default_rng(k * 1000 + n_p)
+    q = g["x"][rng.integers(0, len(g["x"]), nq)] + 0.05 * rng.standard_normal((nq, 128))
+    with w_.catch_warnings():
+        w_.simplefilter("ignore")
+        ids, sc = idx.search_batch(q.reshape(nq, 128), k, n_p)
+    assert ids.shape == (nq, k) and sc.shape == (nq, k)
+    if nq:
+        ref_i, ref_s = o.search_batch(q, k, min(n_p, 64))
+        compare_topk(ids, sc, ref_i, ref_s)
