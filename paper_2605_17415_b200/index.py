@@ -269,7 +269,7 @@ class IvfTqIndex:
         ext = None if external_id is None else np.asarray([external_id], dtype=np.int64)
         return int(self.add_batch(np.asarray(x, dtype=np.float64)[None, :], ext)[0])
 
-    _PIPE_ROWS = 1 << 18  # host->device sub-chunk of a large host batch
+    _PIPE_ROWS = 1 << 17  # host->device sub-chunk of a large host batch (measured best at C2)
 
     def _encode_host_pipelined(self, x: torch.Tensor):
         """Encode a large host (ideally pinned) batch in sub-chunks, copying
