@@ -269,6 +269,7 @@ class IvfTqIndex:
         ext = None if external_id is None else np.asarray([external_id], dtype=np.int64)
         return int(self.add_batch(np.asarray(x, dtype=np.float64)[None, :], ext)[0])
 
+    _QUERY_CHUNK = 1 << 16  # queries per search call (scratch bound)
     _PIPE_ROWS = 1 << 17  # host->device sub-chunk of a large host batch (measured best at C2)
 
     def _encode_host_pipelined(self, x: torch.Tensor):
@@ -324,6 +325,9 @@ class IvfTqIndex:
 
     def add_batch(self, x, external_ids: np.ndarray | None = None) -> np.ndarray:
         """Encode and append rows; returns internal ids (index.py:286-310)."""
+        if (isinstance(x, np.ndarray) and x.ndim == 2 and x.dtype in (np.float32, np.float64)
+                and x.shape[0] > 2 * self._PIPE_ROWS):
+            x = torch.from_numpy(np.ascontiguousarray(x))  # host batch: bounded sub-chunks
         if (isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.dim() == 2
                 and x.shape[1] == self.config.dim and x.shape[0] > 2 * self._PIPE_ROWS
                 and x.dtype in (torch.float32, torch.float64)):
@@ -497,6 +501,19 @@ class IvfTqIndex:
             n_p = self.config.n_lists
         if rerank_depth > 0 and self._raw is None:
             raise ValueError("rerank requires an index built with keep_raw=True")
+        nq_all = (queries.shape[0] if isinstance(queries, torch.Tensor) and queries.dim() == 2
+                  else np.shape(queries)[0] if np.ndim(queries) == 2 else 1)
+        if nq_all > self._QUERY_CHUNK:
+            # bound the per-call scratch (probe scores, pairs, candidate buffers
+            # grow with nq): search in chunks, results in order
+            parts = [self.search_batch(queries[s:s + self._QUERY_CHUNK], k, n_p, rerank_depth,
+                                       return_device=True)
+                     for s in range(0, nq_all, self._QUERY_CHUNK)]
+            ids = torch.cat([p[0] for p in parts])
+            scores = torch.cat([p[1] for p in parts])
+            if return_device:
+                return ids, scores
+            return ids.cpu().numpy(), scores.cpu().numpy()
         qn, bad, nq = self._normalize_queries_device(queries)
         depth = max(k, rerank_depth) if rerank_depth > 0 else k
         dev = self.device

@@ -563,3 +563,16 @@ def test_search_shapes_against_oracle(golden, k, n_p, nq):
     if nq:
         ref_i, ref_s = o.search_batch(q, k, min(n_p, 64))
         compare_topk(ids, sc, ref_i, ref_s)
+
+
+def test_query_chunking_equals_single_call(golden):
+    """Batches above the per-call query chunk are split; results are identical."""
+    g = golden("d128_b4_L64")
+    idx = index_from_golden(g)
+    idx.add_batch(g["x"])
+    q = np.tile(g["queries"], (3, 1))
+    a_i, a_s = idx.search_batch(q, 10, 8)
+    idx._QUERY_CHUNK = 128
+    b_i, b_s = idx.search_batch(q, 10, 8)
+    np.testing.assert_array_equal(a_i, b_i)
+    np.testing.assert_array_equal(a_s, b_s)
