@@ -65,16 +65,25 @@ __device__ __forceinline__ void split16(float x, uint16_t& hi, uint16_t& lo) {
 
 __global__ void prep_stats_kernel(const float* __restrict__ c, int L, int d,
                                   PrepHeader* __restrict__ hdr) {
-  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per centroid (coalesced row reads)
+  const int lane = threadIdx.x & 31;
+  const int l = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (l >= L) return;
   float mx = 0.f, ss = 0.f;
-  for (int j = 0; j < d; ++j) {
+  for (int j = lane; j < d; j += 32) {
     const float v = c[(int64_t)l * d + j];
     mx = fmaxf(mx, fabsf(v));
     ss = fmaf(v, v, ss);
   }
-  atomicMax(&hdr->cmax_abs_bits, __float_as_uint(mx));
-  atomicMax(&hdr->cmax_norm_bits, __float_as_uint(sqrtf(ss) * 1.0001f));
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mx = fmaxf(mx, __shfl_xor_sync(kFull, mx, o));
+    ss += __shfl_xor_sync(kFull, ss, o);
+  }
+  if (lane == 0) {
+    atomicMax(&hdr->cmax_abs_bits, __float_as_uint(mx));
+    atomicMax(&hdr->cmax_norm_bits, __float_as_uint(sqrtf(ss) * 1.0001f));
+  }
 }
 
 // one thread per (centroid, 8-wide k chunk)
@@ -113,6 +122,25 @@ __global__ void prep_c64_kernel(const float* __restrict__ c, int64_t n, double* 
   if (i < n) out[i] = (double)c[i];
 }
 
+// A-operand rows pre-split once per call: x * 2^14 as fp16 hi / lo, packed two
+// per word along k, zero-padded to DP (the same values the kernel's in-place
+// split produces). One thread per word; consecutive threads read consecutive
+// 16-byte pairs of a row.
+__global__ void x_split_kernel(const double* __restrict__ X, int64_t n, int d, int DP,
+                               uint32_t* __restrict__ hi, uint32_t* __restrict__ lo) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int hw = DP / 2;
+  if (i >= n * hw) return;
+  const int64_t r = i / hw;
+  const int k = (int)(i - r * hw) * 2;
+  const double* xr = X + r * (int64_t)d;
+  uint16_t h0, l0, h1, l1;
+  split16(k < d ? (float)(xr[k] * 16384.0) : 0.f, h0, l0);
+  split16(k + 1 < d ? (float)(xr[k + 1] * 16384.0) : 0.f, h1, l1);
+  hi[i] = h0 | ((uint32_t)h1 << 16);
+  lo[i] = l0 | ((uint32_t)l1 << 16);
+}
+
 __device__ __forceinline__ float pick16f(const float (&v)[16], int j) {
   float a[8], b[4], c[2];
 #pragma unroll
@@ -137,7 +165,24 @@ __device__ __forceinline__ float akey_v(uint64_t k) {
 __global__ void __launch_bounds__(kThreads, 1)
 coarse_tc_kernel(const double* __restrict__ X, int64_t n, int d, int DP, int L, int nT,
                  const unsigned char* __restrict__ prep, float* __restrict__ S,
-                 float* __restrict__ top_v, int32_t* __restrict__ top_i) {
+                 float* __restrict__ top_v, int32_t* __restrict__ top_i,
+                 const uint32_t* __restrict__ xs_hi, const uint32_t* __restrict__ xs_lo) {
+  // Work units are (row tile, N tile) pairs in row-major order. With a best-4
+  // output each CTA owns one whole row tile (the epilogue needs every column
+  // of its rows); an S'-only launch splits the units evenly over a grid of
+  // one CTA per SM, so a small query batch (79 row tiles for 10k queries)
+  // still fills all 148 SMs. A CTA's range is a few segments of consecutive
+  // N tiles of one row tile each; the A operand is rebuilt per segment.
+  const int64_t n_rt = (n + kM - 1) / kM;
+  int64_t u0, u1;
+  if (top_v) {
+    u0 = (int64_t)blockIdx.x * nT;
+    u1 = u0 + nT;
+  } else {
+    const int64_t tot = n_rt * nT;
+    u0 = tot * blockIdx.x / gridDim.x;
+    u1 = tot * (blockIdx.x + 1) / gridDim.x;
+  }
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) uint64_t bars[10];
   __shared__ uint32_t tslot;
@@ -150,8 +195,7 @@ coarse_tc_kernel(const double* __restrict__ X, int64_t n, int d, int DP, int L, 
   uint64_t* b_empty = bars + 3;  // [3] MMA commit -> TMA
   uint64_t* acc_full = bars + 6; // [2] MMA commit -> epilogue
   uint64_t* acc_empty = bars + 8;// [2] epilogue -> MMA (count 4)
-  __shared__ __align__(8) uint64_t a_full;
-  const int64_t m0 = (int64_t)blockIdx.x * kM;
+  __shared__ __align__(8) uint64_t a_full, a_empty;
   const uint32_t a_col = 2 * NB;  // A (hi | lo) after the two accumulators
   if (warp == 4) sm100::tmem_alloc(&tslot, 512);
   if (tid == 0) {
@@ -164,6 +208,7 @@ coarse_tc_kernel(const double* __restrict__ X, int64_t n, int d, int DP, int L, 
       sm100::mbar_init(&acc_empty[b], 4);
     }
     sm100::mbar_init(&a_full, 4);
+    sm100::mbar_init(&a_empty, 1);
     sm100::mbar_fence_init();
   }
   sm100::tc_fence_before();
@@ -176,136 +221,180 @@ coarse_tc_kernel(const double* __restrict__ X, int64_t n, int d, int DP, int L, 
     // ---- TMA + MMA issuer (whole warp, elected lane issues) -------------------
     // three operand buffers: tile j+1 is fetched into the buffer tile j-2 used
     // (long retired), so the issuing thread never waits on the MMAs in flight
-    auto load = [&](int j) {
+    const int ng = (int)(u1 - u0);  // tiles of this CTA, in unit order
+    auto load = [&](int g) {
       if (lane == 0) {
-        sm100::mbar_arrive_expect_tx(&b_full[j % 3], tbytes);
-        const unsigned char* src = img + (size_t)j * tbytes;
-        unsigned char* dst = smem + (j % 3) * tbytes;
+        sm100::mbar_arrive_expect_tx(&b_full[g % 3], tbytes);
+        const unsigned char* src = img + (size_t)((u0 + g) % nT) * tbytes;
+        unsigned char* dst = smem + (g % 3) * tbytes;
         for (uint32_t o = 0; o < tbytes; o += 32768)
-          sm100::bulk_g2s(dst + o, src + o, min(32768u, tbytes - o), &b_full[j % 3]);
+          sm100::bulk_g2s(dst + o, src + o, min(32768u, tbytes - o), &b_full[g % 3]);
       }
       __syncwarp();
     };
-    for (int j = 0; j < 3 && j < nT; ++j) load(j);
+    for (int g = 0; g < 3 && g < ng; ++g) load(g);
     const uint32_t idesc = sm100::idesc_f16_f32(kM, NB);
     const uint32_t lbo = NB * 16, sbo = 128;
     const int ks = DP / 16;
-    sm100::mbar_wait(&a_full, 0);
-    for (int j = 0; j < nT; ++j) {
-      if (j >= 2 && j + 1 < nT) {
-        sm100::mbar_wait(&b_empty[(j + 1) % 3], ((j - 2) / 3) & 1);
-        load(j + 1);
-      }
-      const int b = j % 3, ab = j & 1;
-      sm100::mbar_wait(&b_full[b], (j / 3) & 1);
-      if (j >= 2) sm100::mbar_wait(&acc_empty[ab], ((j >> 1) - 1) & 1);
-      sm100::tc_fence_after();
-      const uint32_t bh = sm100::smem_u32(smem + b * tbytes);
-      const uint64_t dh = sm100::smem_desc(bh, lbo, sbo);
-      const uint64_t dl = sm100::smem_desc(bh + DP * NB * 2, lbo, sbo);
-      const uint64_t dstep = (2 * lbo) >> 4;
-      const uint32_t acc = tmem + ab * NB;
-      const uint32_t qh = tmem + a_col, ql = qh + DP / 2;
+    int g = 0, seg = 0;
+    for (int64_t u = u0; u < u1; ++seg) {
+      const int j0 = (int)(u % nT);
+      const int j1 = (int)(u1 - u < (int64_t)(nT - j0) ? j0 + (u1 - u) : nT);
+      u += j1 - j0;
+      sm100::mbar_wait(&a_full, seg & 1);
+      for (int j = j0; j < j1; ++j, ++g) {
+        if (g >= 2 && g + 1 < ng) {
+          sm100::mbar_wait(&b_empty[(g + 1) % 3], ((g - 2) / 3) & 1);
+          load(g + 1);
+        }
+        const int b = g % 3, ab = g & 1;
+        sm100::mbar_wait(&b_full[b], (g / 3) & 1);
+        if (g >= 2) sm100::mbar_wait(&acc_empty[ab], ((g >> 1) - 1) & 1);
+        sm100::tc_fence_after();
+        const uint32_t bh = sm100::smem_u32(smem + b * tbytes);
+        const uint64_t dh = sm100::smem_desc(bh, lbo, sbo);
+        const uint64_t dl = sm100::smem_desc(bh + DP * NB * 2, lbo, sbo);
+        const uint64_t dstep = (2 * lbo) >> 4;
+        const uint32_t acc = tmem + ab * NB;
+        const uint32_t qh = tmem + a_col, ql = qh + DP / 2;
 #pragma unroll 1
-      for (int pass = 0; pass < 3; ++pass) {
-        const uint32_t at = pass == 1 ? ql : qh;
-        const uint64_t db = pass == 2 ? dl : dh;
-        for (int s = 0; s < ks; ++s)
-          sm100::mma_f16_ts_warp(acc, at + s * 8, db + s * dstep, idesc, (pass | s) ? 1u : 0u);
+        for (int pass = 0; pass < 3; ++pass) {
+          const uint32_t at = pass == 1 ? ql : qh;
+          const uint64_t db = pass == 2 ? dl : dh;
+          for (int s = 0; s < ks; ++s)
+            sm100::mma_f16_ts_warp(acc, at + s * 8, db + s * dstep, idesc, (pass | s) ? 1u : 0u);
+        }
+        sm100::mma_commit_warp(&acc_full[ab]);
+        sm100::mma_commit_warp(&b_empty[b]);
       }
-      sm100::mma_commit_warp(&acc_full[ab]);
-      sm100::mma_commit_warp(&b_empty[b]);
+      sm100::mma_commit_warp(&a_empty);  // A is free once this segment's MMAs are done
     }
   } else {
-    // ---- A operand: this thread's row, x * 2^14 split into fp16 hi / lo -------
-    const int64_t r = m0 + tid;
-    const bool live = r < n;
-    const double* xr = X + (r < n ? r : 0) * (int64_t)d;
-    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + a_col;
-    for (int c0 = 0; c0 < DP / 2; c0 += 16) {
-      uint32_t vh[16], vl[16];
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const int k = 2 * (c0 + e);
-        uint16_t h0, l0, h1, l1;
-        split16(live && k < d ? (float)(xr[k] * 16384.0) : 0.f, h0, l0);
-        split16(live && k + 1 < d ? (float)(xr[k + 1] * 16384.0) : 0.f, h1, l1);
-        vh[e] = h0 | ((uint32_t)h1 << 16);
-        vl[e] = l0 | ((uint32_t)l1 << 16);
-      }
-      sm100::tmem_st16(ta + c0, vh);
-      sm100::tmem_st16(ta + DP / 2 + c0, vl);
-    }
-    sm100::tmem_st_wait();
-    sm100::tc_fence_before();
-    __syncwarp();
-    if (lane == 0) sm100::mbar_arrive(&a_full);
-    // ---- epilogue: S' row segments and the row's best kTopA ---------------------
-    uint64_t best[kTopA];
-#pragma unroll
-    for (int p = 0; p < kTopA; ++p) best[p] = 0;
-    for (int j = 0; j < nT; ++j) {
-      const int b = j & 1;
-      sm100::mbar_wait(&acc_full[b], (j >> 1) & 1);
+    int g = 0, seg = 0;
+    for (int64_t u = u0; u < u1; ++seg) {
+      const int64_t rt = u / nT;
+      const int j0 = (int)(u % nT);
+      const int j1 = (int)(u1 - u < (int64_t)(nT - j0) ? j0 + (u1 - u) : nT);
+      u += j1 - j0;
+      // ---- A operand: this thread's row, x * 2^14 split into fp16 hi / lo -----
+      const int64_t r = rt * kM + tid;
+      const bool live = r < n;
+      const double* xr = X + (r < n ? r : 0) * (int64_t)d;
+      const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16) + a_col;
+      if (seg > 0) sm100::mbar_wait(&a_empty, (seg - 1) & 1);
       sm100::tc_fence_after();
-      for (int cc = 0; cc < NB; cc += 32) {
-        uint32_t v[32];
-        sm100::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + b * NB + cc, v);
-        sm100::tmem_ld_wait();
-        if (cc + 32 >= NB) {  // all columns of this accumulator are in registers
-          sm100::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) sm100::mbar_arrive(&acc_empty[b]);
+      if (xs_hi) {
+        // pre-split rows (x_split_kernel): 16-byte loads, all in flight at once
+        const uint4* sh = (const uint4*)(xs_hi + (live ? r : 0) * (int64_t)(DP / 2));
+        const uint4* sl = (const uint4*)(xs_lo + (live ? r : 0) * (int64_t)(DP / 2));
+#pragma unroll 1
+        for (int c0 = 0; c0 < DP / 2; c0 += 32) {
+          uint32_t vh[2][16], vl[2][16];
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              const bool ok = live && c0 + hh * 16 < DP / 2;
+              const int w4 = (c0 + hh * 16) / 4 + x;
+              const uint4 a = ok ? __ldg(sh + w4) : make_uint4(0, 0, 0, 0);
+              const uint4 b = ok ? __ldg(sl + w4) : make_uint4(0, 0, 0, 0);
+              vh[hh][4 * x] = a.x; vh[hh][4 * x + 1] = a.y; vh[hh][4 * x + 2] = a.z; vh[hh][4 * x + 3] = a.w;
+              vl[hh][4 * x] = b.x; vl[hh][4 * x + 1] = b.y; vl[hh][4 * x + 2] = b.z; vl[hh][4 * x + 3] = b.w;
+            }
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh)
+            if (c0 + hh * 16 < DP / 2) {
+              sm100::tmem_st16(ta + c0 + hh * 16, vh[hh]);
+              sm100::tmem_st16(ta + DP / 2 + c0 + hh * 16, vl[hh]);
+            }
         }
-        const int col0 = j * NB + cc;
-        float f[32];
+      } else {
+        for (int c0 = 0; c0 < DP / 2; c0 += 16) {
+          uint32_t vh[16], vl[16];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(v[e]) * inv;
-        if (live && S) {
-          float* dst = S + r * (int64_t)L + col0;
-          if (col0 + 32 <= L && (L & 3) == 0) {
-#pragma unroll
-            for (int e = 0; e < 32; e += 4) *(float4*)(dst + e) = make_float4(f[e], f[e + 1], f[e + 2], f[e + 3]);
-          } else {
-            for (int e = 0; e < 32; ++e)
-              if (col0 + e < L) dst[e] = f[e];
+          for (int e = 0; e < 16; ++e) {
+            const int k = 2 * (c0 + e);
+            uint16_t h0, l0, h1, l1;
+            split16(live && k < d ? (float)(xr[k] * 16384.0) : 0.f, h0, l0);
+            split16(live && k + 1 < d ? (float)(xr[k + 1] * 16384.0) : 0.f, h1, l1);
+            vh[e] = h0 | ((uint32_t)h1 << 16);
+            vl[e] = l0 | ((uint32_t)l1 << 16);
           }
+          sm100::tmem_st16(ta + c0, vh);
+          sm100::tmem_st16(ta + DP / 2 + c0, vl);
         }
-        if (top_v) {
-          // only columns beating the row's current 4th best reach the insert
-          // (columns arrive in ascending order, so an equal value never does);
-          // the warp steps max-over-lanes times per 16-column window
+      }
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&a_full);
+      // ---- epilogue: S' row segments and the row's best kTopA -------------------
+      uint64_t best[kTopA];
 #pragma unroll
-          for (int h = 0; h < 32; h += 16) {
-            const float kth = best[kTopA - 1] ? akey_v(best[kTopA - 1]) : -INFINITY;
-            uint32_t m = 0;
+      for (int p = 0; p < kTopA; ++p) best[p] = 0;
+      for (int j = j0; j < j1; ++j, ++g) {
+        const int b = g & 1;
+        sm100::mbar_wait(&acc_full[b], (g >> 1) & 1);
+        sm100::tc_fence_after();
+        for (int cc = 0; cc < NB; cc += 32) {
+          uint32_t v[32];
+          sm100::tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + b * NB + cc, v);
+          sm100::tmem_ld_wait();
+          if (cc + 32 >= NB) {  // all columns of this accumulator are in registers
+            sm100::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&acc_empty[b]);
+          }
+          const int col0 = j * NB + cc;
+          float f[32];
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-              m |= (col0 + h + e < L && f[h + e] > kth ? 1u : 0u) << e;
-            while (__any_sync(kFull, m != 0)) {
-              const int j = (__ffs(m) - 1) & 15;
-              float w[16];
+          for (int e = 0; e < 32; ++e) f[e] = __uint_as_float(v[e]) * inv;
+          if (live && S) {
+            float* dst = S + r * (int64_t)L + col0;
+            if (col0 + 32 <= L && (L & 3) == 0) {
 #pragma unroll
-              for (int e = 0; e < 16; ++e) w[e] = f[h + e];
-              const uint64_t key = m ? akey(pick16f(w, j), col0 + h + j) : 0ull;
-              m &= m - 1;
-              bool g[kTopA];
+              for (int e = 0; e < 32; e += 4) *(float4*)(dst + e) = make_float4(f[e], f[e + 1], f[e + 2], f[e + 3]);
+            } else {
+              for (int e = 0; e < 32; ++e)
+                if (col0 + e < L) dst[e] = f[e];
+            }
+          }
+          if (top_v) {
+            // only columns beating the row's current 4th best reach the insert
+            // (columns arrive in ascending order, so an equal value never does);
+            // the warp steps max-over-lanes times per 16-column window
 #pragma unroll
-              for (int p = 0; p < kTopA; ++p) g[p] = key > best[p];
+            for (int h = 0; h < 32; h += 16) {
+              const float kth = best[kTopA - 1] ? akey_v(best[kTopA - 1]) : -INFINITY;
+              uint32_t m = 0;
 #pragma unroll
-              for (int p = kTopA - 1; p > 0; --p)
-                best[p] = g[p] ? (g[p - 1] ? best[p - 1] : key) : best[p];
-              best[0] = g[0] ? key : best[0];
+              for (int e = 0; e < 16; ++e)
+                m |= (col0 + h + e < L && f[h + e] > kth ? 1u : 0u) << e;
+              while (__any_sync(kFull, m != 0)) {
+                const int jj = (__ffs(m) - 1) & 15;
+                float w[16];
+#pragma unroll
+                for (int e = 0; e < 16; ++e) w[e] = f[h + e];
+                const uint64_t key = m ? akey(pick16f(w, jj), col0 + h + jj) : 0ull;
+                m &= m - 1;
+                bool gt[kTopA];
+#pragma unroll
+                for (int p = 0; p < kTopA; ++p) gt[p] = key > best[p];
+#pragma unroll
+                for (int p = kTopA - 1; p > 0; --p)
+                  best[p] = gt[p] ? (gt[p - 1] ? best[p - 1] : key) : best[p];
+                best[0] = gt[0] ? key : best[0];
+              }
             }
           }
         }
       }
-    }
-    if (live && top_v) {
+      if (live && top_v) {
 #pragma unroll
-      for (int p = 0; p < kTopA; ++p) {
-        top_v[r * kTopA + p] = best[p] ? akey_v(best[p]) : -INFINITY;
-        top_i[r * kTopA + p] = best[p] ? (int)~(uint32_t)best[p] : -1;
+        for (int p = 0; p < kTopA; ++p) {
+          top_v[r * kTopA + p] = best[p] ? akey_v(best[p]) : -INFINITY;
+          top_i[r * kTopA + p] = best[p] ? (int)~(uint32_t)best[p] : -1;
+        }
       }
     }
   }
@@ -622,10 +711,11 @@ __global__ void __launch_bounds__(256)
 probe_pick_kernel(const double* __restrict__ X, const double* __restrict__ C, int64_t nq, int L,
                   int d, int n_p, const int32_t* __restrict__ cand,
                   const int32_t* __restrict__ cnt, const double* __restrict__ ex,
-                  int32_t* __restrict__ idx_out, double* __restrict__ val_out) {
+                  int32_t* __restrict__ idx_out, double* __restrict__ val_out, bool full_only) {
   const int lane = threadIdx.x & 31;
   const int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r >= nq) return;
+  if (full_only && cnt[r] <= kCandCap) return;  // decided by probe_select_kernel
   WarpQueue<QS> q;
   q.init(n_p);
   const int nc = cnt[r];
@@ -653,6 +743,253 @@ probe_pick_kernel(const double* __restrict__ X, const double* __restrict__ C, in
     if (pos < n_p) {
       idx_out[r * n_p + pos] = q.i[s];
       val_out[r * n_p + pos] = okey_inv(q.k[s]);
+    }
+  }
+}
+
+// ---- fused probe selection: one block (4 warps) per query row -----------------
+// (a) the S' row is staged in shared memory (one coalesced read) while a
+//     256-bin histogram over the fixed range [-R, R] (R bounds |S'| for unit
+//     rows; outliers clamp into the end bins) is built; the bin b holding
+//     the approximate n_p-th value v* is refined by a second 256-bin level
+//     over bin b. With t(v) = (v + R) * scale (one f32 expression, monotone in
+//     v) every value counted at or above (b, sb) has v >= lo = -R +
+//     (b + sb/256) / scale - delta (delta covers the rounding of t), so
+//     v* >= lo;
+// (b) candidates are the columns with S' >= tau = lo - 2 eps: a true member
+//     m of the exact top-n_p has E_m >= E_(n_p) >= v* - eps, hence
+//     S'_m >= v* - 2 eps >= tau;
+// (c) every candidate is scored exactly in f64 (lanes split k, a fixed xor
+//     tree sums the lanes: within a few ulps of the f64 GEMM's sequential
+//     chain, far inside every decision margin);
+// (d) rank selection by (value desc, column asc) -- np.argsort(-C,
+//     kind="stable") (index.py:437-438) -- writes probes and exact values in
+//     order. Rows with more than kCandCap candidates (duplicate centroids),
+//     fewer than n_p (NaN rows) or a degenerate histogram are flagged for
+//     probe_pick_kernel's exact full-row path.
+constexpr int kSelThreads = 128;
+constexpr int kSelRowCap = 16384;  // lists staged per row (larger L: f64 path)
+
+__host__ __device__ inline size_t sel_region_a(int L) {
+  return ((size_t)L * 4 + 15) & ~(size_t)15;
+}
+__host__ __device__ inline size_t sel_smem_bytes(int L, int d) {
+  return sel_region_a(L) + 2 * kBins * 4 + kCandCap * (4 + 8) + (size_t)d * 8;
+}
+
+// warp 0: the bin (from the top) where the cumulative count reaches `need`,
+// and the count strictly above it; -1 if the total is short
+__device__ __forceinline__ int top_bin(const unsigned* h, unsigned need, unsigned& above) {
+  const int lane = threadIdx.x & 31;
+  unsigned own[kBins / 32], tot = 0;
+#pragma unroll
+  for (int i = 0; i < kBins / 32; ++i) {
+    own[i] = h[kBins - 1 - (lane * (kBins / 32) + i)];
+    tot += own[i];
+  }
+  unsigned incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(kFull, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const unsigned ball = __ballot_sync(kFull, incl >= need);
+  if (!ball) return -1;
+  const int owner = __ffs(ball) - 1;
+  int bsel = 0;
+  unsigned abv = 0;
+  if (lane == owner) {
+    unsigned acc = incl - tot;
+#pragma unroll
+    for (int i = 0; i < kBins / 32; ++i) {
+      if (acc + own[i] >= need) {
+        bsel = kBins - 1 - (lane * (kBins / 32) + i);
+        abv = acc;
+        break;
+      }
+      acc += own[i];
+    }
+  }
+  above = __shfl_sync(kFull, abv, owner);
+  return __shfl_sync(kFull, bsel, owner);
+}
+
+__global__ void __launch_bounds__(kSelThreads, 6)
+probe_select_kernel(const float* __restrict__ S, const double* __restrict__ X,
+                    const double* __restrict__ C64, int64_t nq, int L, int d, int n_p,
+                    const unsigned char* __restrict__ prep, int32_t* __restrict__ cnt_out,
+                    int32_t* __restrict__ probe_out, double* __restrict__ coarse_out) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __shared__ int s_nc, s_b, s_need;
+  __shared__ float s_tau;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t r = blockIdx.x;
+  float* srow = (float*)sm;
+  unsigned* hist = (unsigned*)(sm + sel_region_a(L));
+  unsigned* sub = hist + kBins;
+  int* cand = (int*)(sub + kBins);
+  double* ex = (double*)(cand + kCandCap);
+  double* xs = ex + kCandCap;
+  const float* row = S + r * (int64_t)L;
+  const float R = 1.01f * __uint_as_float(((const PrepHeader*)prep)->cmax_norm_bits) + 1e-30f;
+  const float scale = (float)kBins / (2.f * R);
+  auto tmap = [&](float v) { return (v + R) * scale; };
+  auto bin_of = [&](float t) { return min(kBins - 1, max(0, (int)t)); };
+
+  for (int i = tid; i < 2 * kBins; i += kSelThreads) hist[i] = 0;  // both levels
+  for (int k = tid; k < d; k += kSelThreads) xs[k] = X[r * (int64_t)d + k];
+  if (tid == 0) {
+    s_nc = 0;
+    s_b = -1;
+  }
+  __syncthreads();
+  if ((L & 3) == 0) {
+    // 8 row loads in flight per thread before any histogram update
+    constexpr int U = 8;
+    for (int i0 = 0; i0 < L / 4; i0 += U * kSelThreads) {
+      float4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * kSelThreads + tid;
+        v[u] = i < L / 4 ? __ldcs((const float4*)row + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * kSelThreads + tid;
+        if (i < L / 4) {
+          ((float4*)srow)[i] = v[u];
+          atomicAdd(&hist[bin_of(tmap(v[u].x))], 1u);
+          atomicAdd(&hist[bin_of(tmap(v[u].y))], 1u);
+          atomicAdd(&hist[bin_of(tmap(v[u].z))], 1u);
+          atomicAdd(&hist[bin_of(tmap(v[u].w))], 1u);
+        }
+      }
+    }
+  } else {
+    for (int i = tid; i < L; i += kSelThreads) {
+      const float v = __ldcs(row + i);
+      srow[i] = v;
+      atomicAdd(&hist[bin_of(tmap(v))], 1u);
+    }
+  }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned above = 0;
+    const int b = top_bin(hist, (unsigned)n_p, above);
+    if (lane == 0 && b > 0) {  // b == 0 may hold clamped outliers: full path
+      s_b = b;
+      s_need = n_p - (int)above;
+    }
+  }
+  __syncthreads();
+  const int b = s_b;
+  float tau = -INFINITY;
+  if (b > 0) {
+    for (int i = tid; i < L; i += kSelThreads) {
+      const float t = tmap(srow[i]);
+      if (bin_of(t) == b)
+        atomicAdd(&sub[min(kBins - 1, max(0, (int)((t - (float)b) * (float)kBins)))], 1u);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      unsigned above2 = 0;
+      const int sb = max(0, top_bin(sub, (unsigned)s_need, above2));
+      const float delta = R * 0x1p-18f;
+      if (lane == 0)
+        s_tau = -R + ((float)b + (float)sb / (float)kBins) / scale - band(prep) - delta;
+    }
+    __syncthreads();
+    tau = s_tau;
+  }
+  for (int base = 0; base < L; base += kSelThreads) {
+    const int c = base + tid;
+    const bool in = c < L && srow[c] >= tau;
+    const unsigned m = __ballot_sync(kFull, in);
+    int at = 0;
+    if (lane == 0 && m) at = atomicAdd(&s_nc, __popc(m));
+    at = __shfl_sync(kFull, at, 0) + __popc(m & ((1u << lane) - 1u));
+    if (in && at < kCandCap) cand[at] = c;
+  }
+  __syncthreads();
+  const int nc = s_nc;
+  if (nc > kCandCap || nc < n_p) {  // exact full-row path (probe_pick_kernel)
+    if (tid == 0) cnt_out[r] = kCandCap + 1;
+    return;
+  }
+  if (tid == 0) cnt_out[r] = nc;
+  // (c) exact f64 scores: lane l owns k = l + 32 m (x in registers), a warp
+  // scores 8 candidates per step (coalesced 256-byte row loads), and a
+  // butterfly reduce-transpose sums the 8 per-lane partials over the lanes in
+  // the fixed xor-tree order (distance 16, 8, 4, 2, 1) -- deterministic, and
+  // equal rows give equal values
+  {
+    constexpr int kMaxM = 8;  // d <= 256
+    const int M = (d + 31) >> 5;
+    double xr[kMaxM];
+#pragma unroll
+    for (int m = 0; m < kMaxM; ++m) {
+      const int k = lane + 32 * m;
+      xr[m] = (m < M && k < d) ? xs[k] : 0.0;
+    }
+    for (int base = warp * 8; base < nc; base += 4 * 8) {
+      double p[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int ci = base + c < nc ? cand[base + c] : cand[base];
+        const double* crow = C64 + (int64_t)ci * d + lane;
+        double acc = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxM; ++m)
+          if (m < M && lane + 32 * m < d) acc = __fma_rn(xr[m], __ldg(crow + 32 * m), acc);
+        p[c] = acc;
+      }
+      // level 16: keep 4 of 8 (lanes < 16 keep candidates 0-3, others 4-7)
+      const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+      double q4[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double send = u16 ? p[c] : p[c + 4];
+        const double keep = u16 ? p[c + 4] : p[c];
+        q4[c] = keep + __shfl_xor_sync(kFull, send, 16);
+      }
+      double q2[2];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double send = u8 ? q4[c] : q4[c + 2];
+        const double keep = u8 ? q4[c + 2] : q4[c];
+        q2[c] = keep + __shfl_xor_sync(kFull, send, 8);
+      }
+      double q1;
+      {
+        const double send = u4 ? q2[0] : q2[1];
+        const double keep = u4 ? q2[1] : q2[0];
+        q1 = keep + __shfl_xor_sync(kFull, send, 4);
+      }
+      q1 += __shfl_xor_sync(kFull, q1, 2);
+      q1 += __shfl_xor_sync(kFull, q1, 1);
+      // lane holds candidate (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0)
+      const int c = (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
+      if ((lane & 3) == 0 && base + c < nc) ex[base + c] = q1;
+    }
+  }
+  __syncthreads();
+  // (d) rank of each candidate under (value desc, column asc); exact ties
+  // (duplicate centroids) take a second pass over the columns
+  for (int i = tid; i < nc; i += kSelThreads) {
+    const double vi = ex[i];
+    const int ci = cand[i];
+    int rank = 0, eq = 0;
+#pragma unroll 4
+    for (int j = 0; j < nc; ++j) {
+      const double vj = ex[j];  // finite (NaN rows took the full path)
+      rank += vj > vi;
+      eq += vj == vi;
+    }
+    if (eq > 1)
+      for (int j = 0; j < nc; ++j) rank += (ex[j] == vi) & (cand[j] < ci);
+    if (rank < n_p) {
+      probe_out[r * n_p + rank] = ci;
+      coarse_out[r * n_p + rank] = vi;
     }
   }
 }
@@ -692,7 +1029,7 @@ extern "C" int ivftq_coarse_prepare(const float* centroids, int n_lists, int dim
   const int DP = pad_dp(dim);
   const int nT = (n_lists + tile_n(DP) - 1) / tile_n(DP);
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(prep, 0, kHeader, s));
-  prep_stats_kernel<<<(n_lists + 127) / 128, 128, 0, s>>>(centroids, n_lists, dim,
+  prep_stats_kernel<<<(n_lists + 7) / 8, 256, 0, s>>>(centroids, n_lists, dim,
                                                          (PrepHeader*)prep);
   if (int e = check_launch("coarse_prep_stats")) return e;
   const int64_t work = (int64_t)nT * tile_n(DP) * (DP / 8);
@@ -707,7 +1044,18 @@ extern "C" int ivftq_coarse_prepare(const float* centroids, int n_lists, int dim
 
 // S' (optional) and per-row best four (optional) for rows X[0..n)
 static int coarse_gemm(const double* X, int64_t n, int dim, int L, const void* prep, float* S,
-                       float* top_v, int32_t* top_i, cudaStream_t s) {
+                       float* top_v, int32_t* top_i, cudaStream_t s,
+                       uint32_t* xsplit = nullptr) {
+  uint32_t* xh = nullptr;
+  uint32_t* xl = nullptr;
+  if (xsplit) {
+    const int DPx = pad_dp(dim);
+    xh = xsplit;
+    xl = xsplit + (size_t)n * (DPx / 2);
+    const int64_t words = n * (DPx / 2);
+    x_split_kernel<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(X, n, dim, DPx, xh, xl);
+    if (int e = check_launch("x_split")) return e;
+  }
   const int DP = pad_dp(dim);
   const int nT = (L + tile_n(DP) - 1) / tile_n(DP);
   const size_t smem = 3 * tile_bytes(DP) + 1024;
@@ -717,8 +1065,18 @@ static int coarse_gemm(const double* X, int64_t n, int dim, int L, const void* p
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * tile_bytes(128) + 1024)));
     attr = true;
   }
-  coarse_tc_kernel<<<(unsigned)((n + kM - 1) / kM), kThreads, smem, s>>>(
-      X, n, dim, DP, L, nT, (const unsigned char*)prep, S, top_v, top_i);
+  static int n_sms = 0;
+  if (!n_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (n_sms < 1) n_sms = 148;
+  }
+  const int64_t n_rt = (n + kM - 1) / kM;
+  const int64_t units = n_rt * nT;
+  const unsigned grid = top_v ? (unsigned)n_rt : (unsigned)(units < n_sms ? units : n_sms);
+  coarse_tc_kernel<<<grid, kThreads, smem, s>>>(
+      X, n, dim, DP, L, nT, (const unsigned char*)prep, S, top_v, top_i, xh, xl);
   return check_launch("coarse_tc");
 }
 
@@ -763,7 +1121,7 @@ extern "C" int ivftq_assign_tc(const double* xn, const float* centroids, int64_t
 extern "C" size_t ivftq_probe_tc_scratch_bytes(int64_t nq, int n_lists, int dim) {
   // prep | S' (nq*L f32) | cand (nq*cap i32) | ex (nq*cap f64) | cnt (nq i32)
   return ivftq_coarse_prep_bytes(n_lists, dim) + 256 + (size_t)nq * n_lists * 4 + 256 +
-         (size_t)nq * kCandCap * 12 + (size_t)nq * 4 + 1024;
+         (size_t)nq * kCandCap * 12 + (size_t)nq * 4 + 1024 + (size_t)nq * pad_dp(dim) * 4 + 256;
 }
 
 // Tensor-core probes; returns IVFTQ_ERR_UNSUPPORTED when the caller should use f64.
@@ -778,22 +1136,37 @@ int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, 
   float* S = (float*)(ex + nq * kCandCap);
   int32_t* cand = (int32_t*)(S + (((size_t)nq * n_lists + 63) & ~(size_t)63));
   int32_t* cnt = cand + nq * kCandCap;
+  uint32_t* xsplit = (uint32_t*)(((uintptr_t)(cnt + nq) + 255) & ~(uintptr_t)255);
   if (int e = ivftq_coarse_prepare(centroids, n_lists, dim, prep, s)) return e;
-  if (int e = coarse_gemm(qn, nq, dim, n_lists, prep, S, nullptr, nullptr, s)) return e;
+  if (int e = coarse_gemm(qn, nq, dim, n_lists, prep, S, nullptr, nullptr, s, xsplit)) return e;
   const unsigned blocks = (unsigned)((nq + 7) / 8);
-  probe_band_kernel<<<blocks, 256, 0, s>>>(S, nq, n_lists, n_p, prep, cand, cnt);
-  if (int e = check_launch("probe_band")) return e;
   const double* c64 = (const double*)(prep + c64_offset(n_lists, dim));
-  probe_exact_kernel<<<(unsigned)nq, 128, 0, s>>>(qn, c64, nq, dim, cand, cnt, ex);
-  if (int e = check_launch("probe_exact")) return e;
+  const bool fused = n_lists <= kSelRowCap;
+  if (fused) {
+    const size_t sm = sel_smem_bytes(n_lists, dim);
+    static size_t opted = 48 * 1024;
+    if (sm > opted) {
+      IVFTQ_CHECK_CUDA(cudaFuncSetAttribute((const void*)probe_select_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      opted = sm;
+    }
+    probe_select_kernel<<<(unsigned)nq, kSelThreads, sm, s>>>(S, qn, c64, nq, n_lists, dim, n_p,
+                                                             prep, cnt, probe_out, coarse_out);
+    if (int e = check_launch("probe_select")) return e;
+  } else {
+    probe_band_kernel<<<blocks, 256, 0, s>>>(S, nq, n_lists, n_p, prep, cand, cnt);
+    if (int e = check_launch("probe_band")) return e;
+    probe_exact_kernel<<<(unsigned)nq, 128, 0, s>>>(qn, c64, nq, dim, cand, cnt, ex);
+    if (int e = check_launch("probe_exact")) return e;
+  }
   if (n_p <= 32)
     probe_pick_kernel<1><<<blocks, 256, 0, s>>>(qn, c64, nq, n_lists, dim, n_p, cand, cnt,
-                                                ex, probe_out, coarse_out);
+                                                ex, probe_out, coarse_out, fused);
   else if (n_p <= 64)
     probe_pick_kernel<2><<<blocks, 256, 0, s>>>(qn, c64, nq, n_lists, dim, n_p, cand, cnt,
-                                                ex, probe_out, coarse_out);
+                                                ex, probe_out, coarse_out, fused);
   else
     probe_pick_kernel<4><<<blocks, 256, 0, s>>>(qn, c64, nq, n_lists, dim, n_p, cand, cnt,
-                                                ex, probe_out, coarse_out);
+                                                ex, probe_out, coarse_out, fused);
   return check_launch("probe_pick");
 }

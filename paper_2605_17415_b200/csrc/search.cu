@@ -605,14 +605,17 @@ extern "C" int ivftq_probe(const double* qn, const float* centroids, int64_t nq,
     return IVFTQ_ERR_ARG;
   }
   if (nq == 0) return 0;
-  // Path choice (results identical): the tensor-core path pays a dense
-  // tcgen05 GEMM plus an exact f64 re-score of ~n_p gathered centroid rows
-  // per query; the f64 path a dense DFMA GEMM. Measured on B200
-  // (scripts/probe_mode_bench.py, nq = 10k): L=1024 n_p=64: f64 0.24 ms vs
-  // 0.47; L=4096 n_p=32: 0.72 vs 0.52; n_p=128: 0.86 vs 0.88; d=200 n_p=64:
-  // 1.21 vs 0.91 -- so tensor cores when L >= 32 n_p (mode 0), always
-  // (mode 2 / IVFTQ_PROBE_TC=1), never (mode 1).
-  if (probe_tc_enabled() || (probe_tc_auto() && n_lists >= 32 * n_p)) {
+  // Path choice (identical probes; coarse values exact f64 in both, summed in
+  // a different order): the tensor-core path pays a dense tcgen05 GEMM, a
+  // fused per-row selection and an exact f64 re-score of ~n_p gathered
+  // centroid rows per query; the f64 path a dense DFMA GEMM plus a top-n_p
+  // select. Measured on B200 (scripts/probe_mode_bench.py, nq = 10k): L=1024
+  // n_p=64: f64 0.237 ms vs tc 0.171; L=4096 d=96 n_p=32: 0.718 vs 0.250;
+  // n_p=128: 0.850 vs 0.368; d=200 n_p=64: 1.202 vs 0.318 -- so tensor cores
+  // whenever supported (mode 0 / 2 / IVFTQ_PROBE_TC=1), never (mode 1). The
+  // choice never depends on the batch size, so a query's probes and coarse
+  // values do not depend on which batch (or chunk) it arrives in.
+  if (probe_tc_enabled() || probe_tc_auto()) {
     const int e = probe_tc(qn, centroids, nq, n_lists, dim, n_p, probe_out, coarse_out, scratch,
                            scratch_bytes, (cudaStream_t)stream);
     if (e != IVFTQ_ERR_UNSUPPORTED) return e;

@@ -1,5 +1,5 @@
 """Time ivftq_probe (f64 GEMM + select vs tensor-core + exact band) on random
-unit queries/centroids of a given shape; both paths must agree exactly."""
+unit queries/centroids of a given shape; both paths must return identical probes (coarse values to a few ulps)."""
 import sys, time
 from pathlib import Path
 import numpy as np
@@ -20,7 +20,7 @@ for (nq, L, d, n_p) in [(10000, 1024, 128, 64), (10000, 4096, 96, 32), (10000, 4
     sb = L_.ivftq_probe_scratch_bytes(nq, L, d)
     scr = torch.empty(sb, dtype=torch.uint8, device="cuda")
     res = {}
-    for mode in (0, 2):
+    for mode in (1, 2):
         L_.ivftq_set_coarse_mode(mode)
         pr = torch.empty((nq, n_p), dtype=torch.int32, device="cuda")
         co = torch.empty((nq, n_p), dtype=torch.float64, device="cuda")
@@ -34,5 +34,5 @@ for (nq, L, d, n_p) in [(10000, 1024, 128, 64), (10000, 4096, 96, 32), (10000, 4
         e1.record(); torch.cuda.synchronize()
         res[mode] = (e0.elapsed_time(e1) / 5, pr.cpu().numpy(), co.cpu().numpy())
     L_.ivftq_set_coarse_mode(0)
-    same = np.array_equal(res[0][1], res[2][1]) and np.array_equal(res[0][2], res[2][2])
-    print(f"nq={nq} L={L} d={d} n_p={n_p}: f64 {res[0][0]:.3f} ms, tc {res[2][0]:.3f} ms, identical={same}")
+    same = np.array_equal(res[1][1], res[2][1]) and np.allclose(res[1][2], res[2][2], rtol=0, atol=1e-14)
+    print(f"nq={nq} L={L} d={d} n_p={n_p}: f64 {res[1][0]:.3f} ms, tc {res[2][0]:.3f} ms, identical={same}")
