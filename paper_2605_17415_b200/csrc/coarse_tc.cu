@@ -1082,8 +1082,9 @@ static int coarse_gemm(const double* X, int64_t n, int dim, int L, const void* p
 
 extern "C" size_t ivftq_assign_tc_scratch_bytes(int64_t n, int n_lists, int dim) {
   // prep | top_v (n*4 f32) | top_i (n*4 i32) | ex (n*4 f64) | full list (n i32) | count
+  // | pre-split A rows (n * DP * 4)
   return ivftq_coarse_prep_bytes(n_lists, dim) + 256 + (size_t)n * kTopA * 16 + (size_t)n * 4 +
-         1024;
+         1024 + (size_t)n * pad_dp(dim) * 4 + 256;
 }
 
 extern "C" int ivftq_assign_tc(const double* xn, const float* centroids, int64_t n, int n_lists,
@@ -1104,9 +1105,10 @@ extern "C" int ivftq_assign_tc(const double* xn, const float* centroids, int64_t
   int32_t* ti = (int32_t*)(tv + n * kTopA);
   int32_t* full = ti + n * kTopA;
   int32_t* nfull = full + n;
+  uint32_t* xsplit = (uint32_t*)(((uintptr_t)(nfull + 1) + 255) & ~(uintptr_t)255);
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(nfull, 0, sizeof(int32_t), s));
   if (int e = ivftq_coarse_prepare(centroids, n_lists, dim, prep, stream)) return e;
-  if (int e = coarse_gemm(xn, n, dim, n_lists, prep, nullptr, tv, ti, s)) return e;
+  if (int e = coarse_gemm(xn, n, dim, n_lists, prep, nullptr, tv, ti, s, xsplit)) return e;
   const double* c64 = (const double*)(prep + c64_offset(n_lists, dim));
   assign_exact_kernel<<<(unsigned)((n * kTopA + 127) / 128), 128, 0, s>>>(xn, c64, n, dim,
                                                                           prep, tv, ti, ex);

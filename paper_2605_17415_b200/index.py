@@ -204,8 +204,12 @@ class IvfTqIndex:
     # ------------------------------------------------------------------
     # encoding
 
-    def _encode_device(self, x, partition: CoarsePartition | None = None, what="input"):
-        """Run the fused device encoder; returns device (words, lids, norms16, xn)."""
+    def _encode_device(self, x, partition: CoarsePartition | None = None, what="input",
+                       defer_check=False):
+        """Run the fused device encoder; returns device (words, lids, norms16, xn).
+        With defer_check the zero-row flag (first bad row index, n if none) is
+        returned as a device scalar as a fifth element instead of being read
+        here, so a caller pipelining several batches syncs once."""
         cfg = self.config
         cent = self._cent if partition is None else torch.from_numpy(
             np.ascontiguousarray(partition.centroids, np.float32)).to(self.device)
@@ -235,6 +239,8 @@ class IvfTqIndex:
             self._qcent.data_ptr(), xn.data_ptr(), bad.data_ptr(), lids.data_ptr(),
             nrm.data_ptr(), words.data_ptr(), scratch.data_ptr(), sb, _lib.stream_ptr()),
             "encode")
+        if defer_check:
+            return words[:n], lids[:n], nrm[:n], xn, bad
         b = int(bad.item())
         if b < n:
             raise ValueError(f"zero-norm {what} row at index {b}")
@@ -301,22 +307,22 @@ class IvfTqIndex:
         if len(spans) > 1:
             issue(1)
         parts = []
+        flags = []
         keep_xn = self._raw is not None
         for j, (s, e) in enumerate(spans):
             b = j % 2
             cur.wait_event(copied[b])
-            try:
-                words, lids, nrm, xn = self._encode_device(bufs[b][: e - s])
-            except ValueError as err:
-                msg = str(err)
-                if "row at index" in msg:  # report the index within the whole batch
-                    i = int(msg.rsplit(" ", 1)[1])
-                    raise ValueError(f"zero-norm input row at index {s + i}") from None
-                raise
+            words, lids, nrm, xn, bad = self._encode_device(bufs[b][: e - s], defer_check=True)
             freed[b].record(cur)
             if j + 2 < len(spans):
                 issue(j + 2)
             parts.append((words, lids, nrm, xn if keep_xn else None))
+            flags.append(bad)
+        # one sync for the whole batch: the first zero row, with its batch-wide index
+        bad = torch.cat(flags).cpu().numpy()
+        for (s, e), bi in zip(spans, bad):
+            if bi < e - s:
+                raise ValueError(f"zero-norm input row at index {s + int(bi)}")
         words = torch.cat([p[0] for p in parts])
         lids = torch.cat([p[1] for p in parts])
         nrm = torch.cat([p[2] for p in parts])
@@ -524,21 +530,42 @@ class IvfTqIndex:
         coarse = torch.empty((max(nq, 1), n_p), dtype=torch.float64, device=dev)
         pb = self._lib.ivftq_probe_scratch_bytes(nq, L, d)
         pscr = torch.empty(pb, dtype=torch.uint8, device=dev)
+        # the query rotation depends only on qn: it runs on a side stream
+        # while the probe kernels run on the current one
+        qrot = torch.empty((max(nq, 1), d), dtype=torch.float32, device=dev)
+        cur = torch.cuda.current_stream(dev)
+        if getattr(self, "_side_stream", None) is None:
+            self._side_stream = torch.cuda.Stream(device=dev)
+        side = self._side_stream
+        forked, rotated = torch.cuda.Event(), torch.cuda.Event()
+        forked.record(cur)
+        side.wait_event(forked)
+        with torch.cuda.stream(side):
+            self._rotate(qn, nq, qrot)
+            rotated.record(side)
         _lib.check(self._lib.ivftq_probe(qn.data_ptr(), self._cent.data_ptr(), nq, L, d, n_p,
                                          probe.data_ptr(), coarse.data_ptr(), pscr.data_ptr(),
                                          pb, s), "probe")
-        ids, scores = self._scan(qn, nq, probe, coarse, n_p, depth)
+        cur.wait_event(rotated)
+        ids, scores = self._scan(qn, nq, probe, coarse, n_p, depth, qrot)
         if rerank_depth > 0:
             ids, scores = self._rerank(qn, nq, ids, depth, k)
         return self._finish(ids, scores, bad, nq, return_device)
 
-    def _scan(self, qn, nq, probe, coarse, n_p, depth):
+    def _rotate(self, qn, nq, qrot):
+        """Pi q (rotation.py:35-40, index.py:439): f64 product, f32 result."""
+        d = self.config.dim
+        _lib.check(self._lib.ivftq_gemm_nt(qn.data_ptr(), self._R.data_ptr(), _lib.IVFTQ_F64, nq,
+                                           d, d, qrot.data_ptr(), _lib.IVFTQ_F32,
+                                           _lib.stream_ptr()), "rotate")
+
+    def _scan(self, qn, nq, probe, coarse, n_p, depth, qrot=None):
         dev = self.device
         d = self.config.dim
         s = _lib.stream_ptr()
-        qrot = torch.empty((max(nq, 1), d), dtype=torch.float32, device=dev)
-        _lib.check(self._lib.ivftq_gemm_nt(qn.data_ptr(), self._R.data_ptr(), _lib.IVFTQ_F64, nq,
-                                           d, d, qrot.data_ptr(), _lib.IVFTQ_F32, s), "rotate")
+        if qrot is None:
+            qrot = torch.empty((max(nq, 1), d), dtype=torch.float32, device=dev)
+            self._rotate(qn, nq, qrot)
         ids = torch.empty((max(nq, 1), depth), dtype=torch.int64, device=dev)
         scores = torch.empty((max(nq, 1), depth), dtype=torch.float64, device=dev)
         sb = self._lib.ivftq_scan_scratch_bytes(nq, n_p, depth, self.partition.n_lists)
