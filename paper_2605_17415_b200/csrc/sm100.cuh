@@ -45,7 +45,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Same for warps off the critical path: between polls the warp sleeps ~64 ns,
 // so idle roles stop taking issue slots from the busy warps of their SM
 // sub-partition.
-template <int NS = 64>
+#ifndef IVFTQ_WAIT_NS
+#define IVFTQ_WAIT_NS 64
+#endif
+template <int NS = IVFTQ_WAIT_NS>
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"

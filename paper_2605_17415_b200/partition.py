@@ -164,7 +164,7 @@ def train_partition(data: np.ndarray, n_lists: int, seed: int, max_iters: int = 
                            lists=lists)
 
 
-def _train_device(data: np.ndarray, n_lists: int, seed: int, max_iters: int,
+def _train_device(data: np.ndarray, n_lists: int, seed_value: int, max_iters: int,
                   chunk: int = 1 << 16) -> CoarsePartition:
     """The same algorithm and RNG call sequence as the host path, with the data
     resident on the GPU: f64 products through ivftq_gemm_nt, the n-long
@@ -184,7 +184,7 @@ def _train_device(data: np.ndarray, n_lists: int, seed: int, max_iters: int,
     X = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dev)
     n, dim = X.shape
     k = n_lists
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed_value)
 
     def gemm(A, B):
         out = torch.empty((A.shape[0], B.shape[0]), dtype=f64, device=dev)
@@ -206,27 +206,47 @@ def _train_device(data: np.ndarray, n_lists: int, seed: int, max_iters: int,
         return torch.clamp(2.0 - 2.0 * gemm(X, X[torch.as_tensor(rows, device=dev)]), min=0.0)
 
     # ---- k-means++ seeding (partition.py:_kmeanspp) ----
+    # rng.choice(n, size=nc, p=p) draws rng.random(nc) and searches the
+    # normalised cdf of p (side="right"); here the host draws the same
+    # uniforms and the cdf / search / potential / argmin stay on the device.
+    # The fast pass never synchronises; it records each step's potential
+    # total, and a degenerate step (total <= eps: fewer distinct points than
+    # k) re-runs the seeding with the host-checked branch of the reference.
     nc = 2 + int(np.log2(k)) if k > 1 else 1
-    chosen = np.empty(k, dtype=np.int64)
-    chosen[0] = rng.integers(n)
-    d2 = dist2([chosen[0]])[:, 0].contiguous()
-    for j in range(1, k):
-        tot = float(d2.sum().item())
-        if tot <= _EPS:
-            keep = np.ones(n, dtype=bool)
-            keep[chosen[:j]] = False
-            pool = np.flatnonzero(keep)
-            chosen[j] = rng.choice(pool) if len(pool) else rng.integers(n)
-            d2 = torch.minimum(d2, dist2([chosen[j]])[:, 0])
-            continue
-        p = (d2 / tot).cpu().numpy()
-        cand = rng.choice(n, size=nc, p=p / p.sum())
-        cd2 = dist2(cand)
-        pot = torch.minimum(d2[:, None], cd2).sum(dim=0).cpu().numpy()
-        b = int(np.argmin(pot))
-        chosen[j] = cand[b]
-        d2 = torch.minimum(d2, cd2[:, b]).contiguous()
-    cent = X[torch.as_tensor(chosen, device=dev)].clone()
+
+    def seed(rng, checked):
+        chosen = torch.empty(k, dtype=torch.int64, device=dev)
+        tots = torch.empty(k, dtype=f64, device=dev)
+        c0 = int(rng.integers(n))
+        chosen[0] = c0
+        d2 = dist2([c0])[:, 0].contiguous()
+        for j in range(1, k):
+            tot = d2.sum()
+            tots[j] = tot
+            if checked and float(tot.item()) <= _EPS:
+                keep = np.ones(n, dtype=bool)
+                keep[chosen[:j].cpu().numpy()] = False
+                pool = np.flatnonzero(keep)
+                cj = int(rng.choice(pool)) if len(pool) else int(rng.integers(n))
+                chosen[j] = cj
+                d2 = torch.minimum(d2, dist2([cj])[:, 0])
+                continue
+            cdf = torch.cumsum(d2 / tot, 0)
+            cdf /= cdf[-1].clone()
+            u = torch.from_numpy(rng.random(nc)).to(dev, non_blocking=True)
+            cand = torch.clamp(torch.searchsorted(cdf, u, right=True), max=n - 1)
+            cd2 = torch.clamp(2.0 - 2.0 * gemm(X, X[cand]), min=0.0)
+            pot = torch.minimum(d2[:, None], cd2).sum(dim=0)
+            bsel = torch.argmin(pot)  # first minimal index, like np.argmin
+            chosen[j] = cand[bsel]
+            d2 = torch.minimum(d2, cd2.index_select(1, bsel.reshape(1))[:, 0]).contiguous()
+        return chosen, k == 1 or float(tots[1:].min().item()) > _EPS
+
+    chosen, ok = seed(rng, checked=False)
+    if not ok:
+        rng = np.random.default_rng(seed_value)
+        chosen, _ = seed(rng, checked=True)
+    cent = X[chosen].clone()
 
     # ---- Lloyd iterations (partition.py:147-170) ----
     prev = None
