@@ -767,6 +767,9 @@ probe_pick_kernel(const double* __restrict__ X, const double* __restrict__ C, in
 //     order. Rows with more than kCandCap candidates (duplicate centroids),
 //     fewer than n_p (NaN rows) or a degenerate histogram are flagged for
 //     probe_pick_kernel's exact full-row path.
+#ifndef IVFTQ_SEL_MINB
+#define IVFTQ_SEL_MINB 8  // 64 registers: C3 select 142 -> 129 us, C2 123 -> 127
+#endif
 constexpr int kSelThreads = 128;
 constexpr int kSelRowCap = 16384;  // lists staged per row (larger L: f64 path)
 
@@ -814,7 +817,7 @@ __device__ __forceinline__ int top_bin(const unsigned* h, unsigned need, unsigne
   return __shfl_sync(kFull, bsel, owner);
 }
 
-__global__ void __launch_bounds__(kSelThreads, 6)
+__global__ void __launch_bounds__(kSelThreads, IVFTQ_SEL_MINB)
 probe_select_kernel(const float* __restrict__ S, const double* __restrict__ X,
                     const double* __restrict__ C64, int64_t nq, int L, int d, int n_p,
                     const unsigned char* __restrict__ prep, int32_t* __restrict__ cnt_out,
