@@ -68,6 +68,10 @@ const char* ivftq_last_error(void);
 int ivftq_abi_version(void);
 /* Number of kernels this library has launched in the process (bench evidence). */
 unsigned long long ivftq_launch_count(void);
+/* Adds n to that count: the host side calls it on each CUDA-graph replay of
+ * a captured search (n = kernels captured), since a replay launches them
+ * without passing through this library. */
+void ivftq_note_graph_launches(unsigned long long n);
 /* Code layout for (dim, bits, use_sign). */
 int ivftq_code_layout(int dim, int bits, int use_sign, int* field_bits,
                       int* fields_per_word, int* words_per_vec);

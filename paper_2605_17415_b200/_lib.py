@@ -49,6 +49,7 @@ _SIGS = {
     "ivftq_last_error": (C.c_char_p, []),
     "ivftq_abi_version": (_i32, []),
     "ivftq_launch_count": (C.c_ulonglong, []),
+    "ivftq_note_graph_launches": (None, [C.c_ulonglong]),
     "ivftq_code_layout": (_i32, [_i32, _i32, _i32, C.POINTER(_i32), C.POINTER(_i32),
                                  C.POINTER(_i32)]),
     "ivftq_host_double_to_half": (_i32, [_vp, _i64, _vp]),

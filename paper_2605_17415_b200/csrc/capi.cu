@@ -125,6 +125,9 @@ extern "C" int ivftq_abi_version(void) { return IVFTQ_ABI_VERSION; }
 extern "C" unsigned long long ivftq_launch_count(void) {
   return __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
 }
+extern "C" void ivftq_note_graph_launches(unsigned long long n) {
+  __atomic_fetch_add(&g_launches, n, __ATOMIC_RELAXED);
+}
 
 extern "C" int ivftq_code_layout(int dim, int bits, int use_sign, int* fb, int* fpw, int* wpv) {
   if (dim < 1 || bits < 1 || bits > 8) {

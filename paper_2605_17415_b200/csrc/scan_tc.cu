@@ -1182,9 +1182,17 @@ static int launch_tc(const Params& P, size_t smem, int grid, cudaStream_t s) {
     set_error("scan_tc: smem %zu rejected: %s", smem, cudaGetErrorString(e));
     return IVFTQ_ERR_UNSUPPORTED;
   }
-  if (g_time_kernel) cudaEventRecord(g_ev[0], s);
+  // inside a stream capture (IvfTqIndex's graph path) the records must be
+  // external event nodes to mark the kernel at every replay
+  unsigned rec_flags = cudaEventRecordDefault;
+  if (g_time_kernel) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive) rec_flags = cudaEventRecordExternal;
+    cudaEventRecordWithFlags(g_ev[0], s, rec_flags);
+  }
   fn<<<grid, kThreads, smem, s>>>(P);
-  if (g_time_kernel) cudaEventRecord(g_ev[1], s);
+  if (g_time_kernel) cudaEventRecordWithFlags(g_ev[1], s, rec_flags);
   return check_launch("scan_tc");
 }
 
@@ -1213,25 +1221,38 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   int64_t np = nq * n_p;
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(S.cnt2, 0, S.zero_end - (char*)S.cnt2, s));
   unsigned gp = (unsigned)((np + 255) / 256);
+  // The seeded bounds and the probe regrouping both only read the probes:
+  // the seeding runs on a side stream, overlapping the (latency-bound,
+  // partly single-block) regroup kernels, and the scan waits for both.
+  static cudaStream_t side = nullptr;
+  static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  if (!side) {
+    IVFTQ_CHECK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    IVFTQ_CHECK_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    IVFTQ_CHECK_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+  }
+  IVFTQ_CHECK_CUDA(cudaEventRecord(fork_ev, s));
+  IVFTQ_CHECK_CUDA(cudaStreamWaitEvent(side, fork_ev, 0));
   // global pruning bounds: seeded from each query's nearest list (exactness
   // preserved by a margin), unless disabled for measurement
   if (getenv("IVFTQ_NO_SEED")) {
-    thr_init_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, s>>>(S.thr_key, nq);
+    thr_init_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, side>>>(S.thr_key, nq);
   } else {
     const char* sp_env = getenv("IVFTQ_SEED_P");
     const int sp = sp_env ? atoi(sp_env) : 1;
     const unsigned sb = (unsigned)((nq + 7) / 8);
     if (sp >= 4)
-      seed_bound_kernel<4><<<sb, 256, 0, s>>>(*st, probe, coarse, qrot, levels, nq, n_p, depth,
-                                              S.thr_key);
+      seed_bound_kernel<4><<<sb, 256, 0, side>>>(*st, probe, coarse, qrot, levels, nq, n_p,
+                                                 depth, S.thr_key);
     else if (sp == 2)
-      seed_bound_kernel<2><<<sb, 256, 0, s>>>(*st, probe, coarse, qrot, levels, nq, n_p, depth,
-                                              S.thr_key);
+      seed_bound_kernel<2><<<sb, 256, 0, side>>>(*st, probe, coarse, qrot, levels, nq, n_p,
+                                                 depth, S.thr_key);
     else
-      seed_bound_kernel<1><<<sb, 256, 0, s>>>(*st, probe, coarse, qrot, levels, nq, n_p, depth,
-                                              S.thr_key);
+      seed_bound_kernel<1><<<sb, 256, 0, side>>>(*st, probe, coarse, qrot, levels, nq, n_p,
+                                                 depth, S.thr_key);
   }
   if (int e = check_launch("thr_init")) return e;
+  IVFTQ_CHECK_CUDA(cudaEventRecord(join_ev, side));
   pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.cnt2);
   if (int e = check_launch("pair_count")) return e;
   pair_scan_kernel<<<1, 1024, 0, s>>>(S.cnt2, L, S.pstart2, S.pstart, S.ntile, S.G, S.n_items);
@@ -1250,6 +1271,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
     q16_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(qrot, nq, st->dim, DP, S.q_hi, S.q_lo);
     if (int e = check_launch("q16")) return e;
   }
+  IVFTQ_CHECK_CUDA(cudaStreamWaitEvent(s, join_ev, 0));  // seeded bounds are in place
   Params P{};
   const int kmax = kmax_for(depth);
   pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS, &P.nAcc);

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import hashlib
+import os
 import warnings
 from dataclasses import dataclass
 
@@ -520,8 +521,61 @@ class IvfTqIndex:
             if return_device:
                 return ids, scores
             return ids.cpu().numpy(), scores.cpu().numpy()
-        qn, bad, nq = self._normalize_queries_device(queries)
         depth = max(k, rerank_depth) if rerank_depth > 0 else k
+        if self._graph_eligible(queries):
+            ids, scores, bad = self._search_graphed(queries, k, n_p, depth, rerank_depth)
+            nq = queries.shape[0]
+            if return_device:  # the graph's outputs are overwritten by its next replay
+                ids, scores = ids.clone(), scores.clone()
+            return self._finish(ids, scores, bad, nq, return_device)
+        ids, scores, bad, nq = self._search_core(queries, k, n_p, depth, rerank_depth)
+        return self._finish(ids, scores, bad, nq, return_device)
+
+    # Repeated searches of one shape replay a CUDA graph of the whole device
+    # sequence (normalize, probe, rotate, regroup, seed, scan, merge): one
+    # launch instead of ~30, no host work between kernels. Graphs are keyed by
+    # (rows, dtype, k, n_p, depth, rerank) and dropped whenever the index
+    # changes (they hold its buffer pointers).
+    use_graphs = os.environ.get("IVFTQ_NO_GRAPH", "") != "1"
+    _MAX_GRAPHS = 8
+
+    def _graph_eligible(self, queries) -> bool:
+        return (self.use_graphs and isinstance(queries, torch.Tensor) and queries.dim() == 2
+                and queries.dtype in (torch.float32, torch.float64)
+                and queries.shape[1] == self.config.dim
+                and 1 <= queries.shape[0] <= self._QUERY_CHUNK)
+
+    def _search_graphed(self, queries, k, n_p, depth, rerank_depth):
+        if getattr(self, "_graph_version", None) != self._version:
+            self._graphs = {}
+            self._graph_version = self._version
+        key = (tuple(queries.shape), queries.dtype, k, n_p, depth, rerank_depth, self.scan_mode)
+        ent = self._graphs.pop(key, None)
+        if ent is not None:
+            self._graphs[key] = ent  # most recently used last
+            ent[1].copy_(queries, non_blocking=True)
+        else:
+            while len(self._graphs) >= self._MAX_GRAPHS:  # bound the graphs' memory pools
+                self._graphs.pop(next(iter(self._graphs)))
+            static_in = torch.empty(queries.shape, dtype=queries.dtype, device=self.device)
+            static_in.copy_(queries)
+            # warm-up outside capture: library lazy state, allocator pools
+            self._search_core(static_in, k, n_p, depth, rerank_depth)
+            torch.cuda.synchronize(self.device)
+            g = torch.cuda.CUDAGraph()
+            c0 = self._lib.ivftq_launch_count()
+            with torch.cuda.graph(g):
+                out = self._search_core(static_in, k, n_p, depth, rerank_depth)[:3]
+            ent = (g, static_in, out, self._lib.ivftq_launch_count() - c0)
+            self._graphs[key] = ent
+        g, _, out, n_launch = ent
+        g.replay()
+        self._lib.ivftq_note_graph_launches(n_launch)
+        return out
+
+    def _search_core(self, queries, k, n_p, depth, rerank_depth):
+        """The device sequence of one search (no host synchronisation)."""
+        qn, bad, nq = self._normalize_queries_device(queries)
         dev = self.device
         L = self.partition.n_lists
         d = self.config.dim
@@ -550,7 +604,7 @@ class IvfTqIndex:
         ids, scores = self._scan(qn, nq, probe, coarse, n_p, depth, qrot)
         if rerank_depth > 0:
             ids, scores = self._rerank(qn, nq, ids, depth, k)
-        return self._finish(ids, scores, bad, nq, return_device)
+        return ids, scores, bad, nq
 
     def _rotate(self, qn, nq, qrot):
         """Pi q (rotation.py:35-40, index.py:439): f64 product, f32 result."""

@@ -594,3 +594,44 @@ def test_query_chunking_equals_single_call(golden):
     b_i, b_s = idx.search_batch(q, 10, 8)
     np.testing.assert_array_equal(a_i, b_i)
     np.testing.assert_array_equal(a_s, b_s)
+
+
+def test_graph_replay_equals_eager(golden):
+    """Repeated same-shape searches replay a captured CUDA graph: results equal
+    the eager path call after call, with fresh inputs, and the graphs are
+    dropped (re-captured) once the index changes."""
+    import torch
+
+    g = golden("d128_b4_L64")
+    idx = index_from_golden(g)
+    half = len(g["x"]) // 2
+    idx.add_batch(g["x"][:half])
+    rng = np.random.default_rng(5)
+
+    def both(q):
+        qt = torch.from_numpy(q).cuda()
+        idx.use_graphs = False
+        e = idx.search_batch(qt, 10, 8)
+        idx.use_graphs = True
+        r = idx.search_batch(qt, 10, 8)
+        return e, r
+
+    for _ in range(3):  # capture, then replays with new inputs
+        q = g["x"][rng.integers(0, half, 300)] + 0.05 * rng.standard_normal((300, 128))
+        (ei, es), (ri, rs) = both(q)
+        np.testing.assert_array_equal(ei, ri)
+        np.testing.assert_array_equal(es, rs)
+    assert len(idx._graphs) == 1
+    dev_ids, _ = idx.search_batch(torch.from_numpy(q).cuda(), 10, 8, return_device=True)
+    idx.search_batch(torch.from_numpy(q[::-1].copy()).cuda(), 10, 8)  # next replay
+    np.testing.assert_array_equal(dev_ids.cpu().numpy(), ei)  # returned tensors are owned
+    idx.add_batch(g["x"][half:])  # index changed: graphs re-captured
+    q = g["x"][rng.integers(0, len(g["x"]), 300)]
+    (ei, es), (ri, rs) = both(q)
+    np.testing.assert_array_equal(ei, ri)
+    np.testing.assert_array_equal(es, rs)
+    assert ei.max() >= half  # the new rows are searched
+    with pytest.raises(ValueError, match="zero-norm"):
+        z = torch.from_numpy(q).cuda().clone()
+        z[7] = 0
+        idx.search_batch(z, 10, 8)
