@@ -13,6 +13,7 @@ built library the compute methods raise.
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import hashlib
 import os
 import warnings
@@ -158,7 +159,7 @@ class IvfTqIndex:
         self._list_of = _Grow((), torch.int32, dev, 0)
         self._norm_of = _Grow((), torch.int16, dev, 0)
         self._raw = _Grow((d,), torch.float32, dev) if config.keep_raw else None
-        self._ext = np.zeros(1024, dtype=np.int64)
+        self._ext = None  # external ids; None while every one equals its internal id
         self._count = 0
         self._version = 0
         self._host_cache: dict = {}
@@ -342,19 +343,23 @@ class IvfTqIndex:
         else:
             words, lids, nrm, xn = self._encode_device(x)
         n = words.shape[0]
-        if external_ids is None:
-            external_ids = np.arange(self._count, self._count + n, dtype=np.int64)
-        else:
+        if external_ids is not None:
             external_ids = np.asarray(external_ids, dtype=np.int64)
             if len(external_ids) != n:
                 raise ValueError("external_ids length mismatch")
         self._append_encoded(words, lids, nrm, xn)
         first = self._count - n
-        if len(self._ext) < self._count:
-            g = np.zeros(max(self._count, 2 * len(self._ext)), dtype=np.int64)
-            g[:first] = self._ext[:first]
-            self._ext = g
-        self._ext[first:self._count] = external_ids
+        # external ids default to the internal ones (index.py:299-303); while
+        # every id so far is a default, none is stored (_ext is None)
+        if external_ids is not None and self._ext is None:
+            self._ext = np.arange(max(self._count, 1024), dtype=np.int64)
+        if self._ext is not None:
+            if len(self._ext) < self._count:
+                g = np.zeros(max(self._count, 2 * len(self._ext)), dtype=np.int64)
+                g[:first] = self._ext[:first]
+                self._ext = g
+            self._ext[first:self._count] = (np.arange(first, self._count, dtype=np.int64)
+                                            if external_ids is None else external_ids)
         return np.arange(first, first + n, dtype=np.int64)
 
     def _append_encoded(self, words, lids, nrm, xn):
@@ -432,6 +437,8 @@ class IvfTqIndex:
 
     @property
     def external_ids(self) -> np.ndarray:
+        if self._ext is None:
+            return np.arange(self._count, dtype=np.int64)
         return self._ext[: self._count]
 
     @property
@@ -523,11 +530,22 @@ class IvfTqIndex:
             return ids.cpu().numpy(), scores.cpu().numpy()
         depth = max(k, rerank_depth) if rerank_depth > 0 else k
         if self._graph_eligible(queries):
-            ids, scores, bad = self._search_graphed(queries, k, n_p, depth, rerank_depth)
-            nq = queries.shape[0]
-            if return_device:  # the graph's outputs are overwritten by its next replay
-                ids, scores = ids.clone(), scores.clone()
-            return self._finish(ids, scores, bad, nq, return_device)
+            if isinstance(queries, np.ndarray):
+                queries = torch.from_numpy(np.ascontiguousarray(queries))
+            try:
+                ids, scores, bad = self._search_graphed(queries, k, n_p, depth, rerank_depth)
+            except (RuntimeError, _lib.IvftqError) as err:  # capture refused: run eagerly
+                if "captur" not in str(err):
+                    raise
+                warnings.warn(f"CUDA graph capture failed ({err}); searching without graphs",
+                              stacklevel=2)
+                self.use_graphs = False
+                torch.cuda.synchronize(self.device)
+            else:
+                nq = queries.shape[0]
+                if return_device:  # the graph's outputs are overwritten by its next replay
+                    ids, scores = ids.clone(), scores.clone()
+                return self._finish(ids, scores, bad, nq, return_device)
         ids, scores, bad, nq = self._search_core(queries, k, n_p, depth, rerank_depth)
         return self._finish(ids, scores, bad, nq, return_device)
 
@@ -540,6 +558,8 @@ class IvfTqIndex:
     _MAX_GRAPHS = 8
 
     def _graph_eligible(self, queries) -> bool:
+        if isinstance(queries, np.ndarray) and queries.dtype in (np.float32, np.float64):
+            queries = torch.from_numpy(queries)  # a view; copied into the graph input
         return (self.use_graphs and isinstance(queries, torch.Tensor) and queries.dim() == 2
                 and queries.dtype in (torch.float32, torch.float64)
                 and queries.shape[1] == self.config.dim
@@ -564,8 +584,16 @@ class IvfTqIndex:
             torch.cuda.synchronize(self.device)
             g = torch.cuda.CUDAGraph()
             c0 = self._lib.ivftq_launch_count()
-            with torch.cuda.graph(g):
-                out = self._search_core(static_in, k, n_p, depth, rerank_depth)[:3]
+            # no garbage collection inside the capture: a collected pinned
+            # buffer would record a CUDA event on the capturing stream
+            gc_on = gc.isenabled()
+            gc.disable()
+            try:
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                    out = self._search_core(static_in, k, n_p, depth, rerank_depth)[:3]
+            finally:
+                if gc_on:
+                    gc.enable()
             ent = (g, static_in, out, self._lib.ivftq_launch_count() - c0)
             self._graphs[key] = ent
         g, _, out, n_launch = ent
