@@ -198,6 +198,9 @@ int ivftq_scan_topk_tc(const ivftq_store* store, const int32_t* probe, const dou
 /* Instrumentation: bracket the tensor-core scan kernel with CUDA events on its
  * stream; ivftq_last_scan_kernel_ms() syncs and returns the last duration. */
 int ivftq_set_kernel_timing(int on);
+/* Current timing switch (a captured search graph records the events only if
+ * it was captured with timing on; the host keys its graphs on this). */
+int ivftq_get_kernel_timing(void);
 double ivftq_last_scan_kernel_ms(void);
 /* Exact re-score of the top-depth candidates against the raw f32 store and
  * re-order to top-k (index.py:470-473). */

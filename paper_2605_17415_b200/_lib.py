@@ -85,6 +85,7 @@ _SIGS = {
     "ivftq_scan_topk_tc": (_i32, [C.POINTER(IvftqStore), _vp, _vp, _vp, _vp, _i64, _i32, _i32,
                                   _vp, _vp, _vp, _sz, _vp]),
     "ivftq_scan_tc_supported": (_i32, [_i32, _i32, _i32]),
+    "ivftq_get_kernel_timing": (_i32, []),
     "ivftq_set_kernel_timing": (_i32, [_i32]),
     "ivftq_last_scan_kernel_ms": (C.c_double, []),
     "ivftq_scan_tc_scratch_bytes": (_sz, [_i64, _i32, _i32, _i32]),

@@ -173,6 +173,26 @@ __device__ double pw_sumsq(Load ld, int n) {
   return ret;
 }
 
+// The same sum for one row in shared memory, computed by the 8 lanes of an
+// aligned lane group when n <= kPwBlock: lane j runs numpy's accumulator r_j
+// (elements j, j+8, ...), three xor shuffles form ((r0+r1)+(r2+r3)) +
+// ((r4+r5)+(r6+r7)) exactly as pw_block does (IEEE addition is commutative,
+// so every lane of the group ends with the same bits), then the n % 8 tail.
+// Longer or shorter rows take the serial form in every lane of the group.
+__device__ __forceinline__ double pw_sumsq_lane8(const double* rp, int n) {
+  const int lane = threadIdx.x & 31, j = lane & 7;
+  const unsigned gm = 0xffu << (lane & 24);
+  if (n > kPwBlock || n < 8) return pw_sumsq([&](int i) { return rp[i]; }, n);
+  const int lim = n - (n % 8);
+  double r = sq(rp[j]);
+  for (int i = 8; i < lim; i += 8) r = add(r, sq(rp[i + j]));
+  r = add(r, __shfl_xor_sync(gm, r, 1));
+  r = add(r, __shfl_xor_sync(gm, r, 2));
+  r = add(r, __shfl_xor_sync(gm, r, 4));
+  for (int i = lim; i < n; ++i) r = add(r, sq(rp[i]));
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // Code layout helpers. One "field" per coordinate: c = bin*2 + sign,
 // `field_bits` = bits + 1 wide, `fields_per_word` per uint32. The sign bit is

@@ -30,12 +30,15 @@ normalize_kernel(const T* __restrict__ x, int64_t n, int d, double* __restrict__
     sm[r * ld + c] = (double)x[(row0 + r) * d + c];
   }
   __syncthreads();
-  if (threadIdx.x < rows) {
-    const double* rp = sm + threadIdx.x * ld;
-    double s = pw_sumsq([&](int i) { return rp[i]; }, d);
-    double nr = __dsqrt_rn(s);
-    nrm[threadIdx.x] = nr;
-    if (!(nr >= 1e-12) && !(nr != nr)) atomicMin(bad, (unsigned long long)(row0 + threadIdx.x));
+  // 8 lanes per row (whole lane groups iterate together: rows is uniform)
+  for (int r = threadIdx.x >> 3; r < ((rows + 3) & ~3); r += kRowThreads / 8) {
+    const int rr = r < rows ? r : 0;
+    const double s = pw_sumsq_lane8(sm + rr * ld, d);
+    if ((threadIdx.x & 7) == 0 && r < rows) {
+      const double nr = __dsqrt_rn(s);
+      nrm[r] = nr;
+      if (!(nr >= 1e-12) && !(nr != nr)) atomicMin(bad, (unsigned long long)(row0 + r));
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < rows * d; i += blockDim.x) {
@@ -62,10 +65,10 @@ residual_kernel(const double* __restrict__ xn, const float* __restrict__ cent,
     out[(row0 + r) * d + c] = v;
   }
   __syncthreads();
-  if (threadIdx.x < rows) {
-    const double* rp = sm + threadIdx.x * ld;
-    double s = pw_sumsq([&](int i) { return rp[i]; }, d);
-    norm_out[row0 + threadIdx.x] = d2h_bits(__dsqrt_rn(s));
+  for (int r = threadIdx.x >> 3; r < ((rows + 3) & ~3); r += kRowThreads / 8) {
+    const int rr = r < rows ? r : 0;
+    const double s = pw_sumsq_lane8(sm + rr * ld, d);
+    if ((threadIdx.x & 7) == 0 && r < rows) norm_out[row0 + r] = d2h_bits(__dsqrt_rn(s));
   }
 }
 
@@ -102,10 +105,10 @@ quantize_pack_kernel(const double* __restrict__ rot, const uint16_t* __restrict_
     sm[r * ld + c] = rot[(row0 + r) * d + c];
   }
   __syncthreads();
-  if (threadIdx.x < rows) {
-    const double* rp = sm + threadIdx.x * ld;
-    double s = pw_sumsq([&](int i) { return rp[i]; }, d);
-    nrm[threadIdx.x] = __dsqrt_rn(s);
+  for (int r = threadIdx.x >> 3; r < ((rows + 3) & ~3); r += kRowThreads / 8) {
+    const int rr = r < rows ? r : 0;
+    const double s = pw_sumsq_lane8(sm + rr * ld, d);
+    if ((threadIdx.x & 7) == 0 && r < rows) nrm[r] = __dsqrt_rn(s);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < rows * W; i += blockDim.x) {

@@ -1075,11 +1075,18 @@ extern "C" int ivftq_set_kernel_timing(int on) {
   return 0;
 }
 
+extern "C" int ivftq_get_kernel_timing(void) { return g_time_kernel ? 1 : 0; }
+
 extern "C" double ivftq_last_scan_kernel_ms(void) {
   if (!g_ev[0]) return -1.0;
   float ms = -1.f;
-  if (cudaEventSynchronize(g_ev[1]) != cudaSuccess) return -1.0;
-  if (cudaEventElapsedTime(&ms, g_ev[0], g_ev[1]) != cudaSuccess) return -1.0;
+  // events never recorded (no timed launch yet) fail here: report -1 and
+  // clear the error so it does not surface at the next launch check
+  if (cudaEventSynchronize(g_ev[1]) != cudaSuccess ||
+      cudaEventElapsedTime(&ms, g_ev[0], g_ev[1]) != cudaSuccess) {
+    cudaGetLastError();
+    return -1.0;
+  }
   return ms;
 }
 

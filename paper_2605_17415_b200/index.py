@@ -569,7 +569,8 @@ class IvfTqIndex:
         if getattr(self, "_graph_version", None) != self._version:
             self._graphs = {}
             self._graph_version = self._version
-        key = (tuple(queries.shape), queries.dtype, k, n_p, depth, rerank_depth, self.scan_mode)
+        key = (tuple(queries.shape), queries.dtype, k, n_p, depth, rerank_depth, self.scan_mode,
+               self._lib.ivftq_get_kernel_timing())
         ent = self._graphs.pop(key, None)
         if ent is not None:
             self._graphs[key] = ent  # most recently used last

@@ -635,3 +635,30 @@ def test_graph_replay_equals_eager(golden):
         z = torch.from_numpy(q).cuda().clone()
         z[7] = 0
         idx.search_batch(z, 10, 8)
+
+
+def test_graph_replay_with_kernel_timing(golden):
+    """Toggling the scan-kernel timing between graph replays: the timed search
+    reports a kernel time (its graph is captured with the events), and
+    searches of other shapes afterwards still run (no stale CUDA error)."""
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+
+    g = golden("d128_b4_L64")
+    idx = index_from_golden(g)
+    idx.add_batch(g["x"])
+    q = torch.from_numpy(g["x"][:512] + 0.01).cuda()
+    lib = _lib.lib()
+    idx.search_batch(q, 10, 8, return_device=True)
+    lib.ivftq_set_kernel_timing(1)
+    try:
+        idx.search_batch(q, 10, 8, return_device=True)
+        ms = lib.ivftq_last_scan_kernel_ms()
+    finally:
+        lib.ivftq_set_kernel_timing(0)
+    assert ms > 0
+    a = idx.search_batch(q[:300], 10, 16)
+    idx.use_graphs = False
+    b = idx.search_batch(q[:300], 10, 16)
+    np.testing.assert_array_equal(a[0], b[0])
