@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples of one kernel to CUDA source lines.
 
-usage: python scripts/ncu_lines.py report.ncu-rep <cubin> <mangled-kernel-name> [top]
+usage: python scripts/ncu_lines.py report.ncu-rep <cubin> <mangled-kernel-name> [top] [kernel-regex]
 
 The report's SASS source page (ncu --page source --print-source sass) gives
 per-instruction stall samples by absolute address; `nvdisasm -g` on the
@@ -37,8 +37,10 @@ def line_map(cubin, fn):
 def main():
     rep, cubin, fn = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
-                          ], capture_output=True, text=True).stdout
+    # optional 5th argument: kernel-name regex, for reports holding several kernels
+    filt = ["-k", "regex:" + sys.argv[5]] if len(sys.argv) > 5 else []
+    txt = subprocess.run(["ncu", "-i", rep, *filt, "--page", "source", "--csv", "--print-source",
+                          "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr = rows[1]
     ia, iex, isrc = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Source")

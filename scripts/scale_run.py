@@ -90,6 +90,11 @@ def main():
     # ---- ingest from pinned host rows -----------------------------------------
     chunk = 1_000_000
     pinned = torch.from_numpy(base).pin_memory()
+    # warm-up on a throwaway index: lazy kernel loading and first-use
+    # allocations stay out of the timed region
+    warm = IvfTqIndex(cfg, q, R, CoarsePartition(w.n_lists, w.d, cent), device=dev)
+    warm.add_batch(pinned[:300_000])
+    del warm
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.time()
