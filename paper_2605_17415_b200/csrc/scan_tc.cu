@@ -1259,6 +1259,13 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
                                                  depth, S.thr_key);
   }
   if (int e = check_launch("thr_init")) return e;
+  {  // the scan's A-operand rows (fp16 hi/lo of the rotated queries), also off the main stream
+    const int DPq = pad_dp(st->dim);
+    const int64_t nw = nq * (DPq / 2);
+    q16_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, side>>>(qrot, nq, st->dim, DPq, S.q_hi,
+                                                                S.q_lo);
+    if (int e = check_launch("q16")) return e;
+  }
   IVFTQ_CHECK_CUDA(cudaEventRecord(join_ev, side));
   pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.cnt2);
   if (int e = check_launch("pair_count")) return e;
@@ -1273,12 +1280,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
 
   const int fb = st->field_bits, C = 1 << fb;
   const int DP = pad_dp(st->dim);
-  {
-    const int64_t nw = nq * (DP / 2);
-    q16_kernel<<<(unsigned)((nw + 255) / 256), 256, 0, s>>>(qrot, nq, st->dim, DP, S.q_hi, S.q_lo);
-    if (int e = check_launch("q16")) return e;
-  }
-  IVFTQ_CHECK_CUDA(cudaStreamWaitEvent(s, join_ev, 0));  // seeded bounds are in place
+  IVFTQ_CHECK_CUDA(cudaStreamWaitEvent(s, join_ev, 0));  // seeded bounds, A rows in place
   Params P{};
   const int kmax = kmax_for(depth);
   pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS, &P.nAcc);

@@ -662,3 +662,27 @@ def test_graph_replay_with_kernel_timing(golden):
     idx.use_graphs = False
     b = idx.search_batch(q[:300], 10, 16)
     np.testing.assert_array_equal(a[0], b[0])
+
+
+def test_external_ids_default_and_custom(golden, tmp_path):
+    """External ids default to the internal ones (index.py:299-303) and are
+    only materialised once a caller passes its own; mixed batches, search
+    results (internal ids) and save/load keep them."""
+    from paper_2605_17415_b200.storage import load_index, save_index
+
+    g = golden("d32_b4_L16_raw")
+    idx = index_from_golden(g)
+    x = g["x"]
+    assert idx.add_batch(x[:100]).tolist() == list(range(100))
+    assert idx._ext is None
+    np.testing.assert_array_equal(idx.external_ids, np.arange(100))
+    idx.add_batch(x[100:150], external_ids=np.arange(1000, 1050))
+    idx.add_batch(x[150:200])
+    want = np.concatenate([np.arange(100), np.arange(1000, 1050), np.arange(150, 200)])
+    np.testing.assert_array_equal(idx.external_ids, want)
+    assert idx.add(x[200], external_id=77) == 200
+    np.testing.assert_array_equal(idx.external_ids[-1:], [77])
+    p = tmp_path / "ext.ivtq"
+    save_index(idx, p)
+    back = load_index(p)
+    np.testing.assert_array_equal(back.external_ids, idx.external_ids)
