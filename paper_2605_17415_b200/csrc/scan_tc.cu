@@ -58,8 +58,14 @@ constexpr int kM = 128;          // queries per item = MMA M
 constexpr int kProdWarp = 0;     // producer (TMA + control records)
 constexpr int kMmaWarp = 1;      // tcgen05.mma issuer, owns TMEM
 constexpr int kDecWarp0 = 2;     // decoder warps 2..9
-constexpr int kDecWarps = 8;
-constexpr int kEpiWarp0 = 10;    // epilogue warps 10..17
+#ifndef IVFTQ_DEC_WARPS
+#define IVFTQ_DEC_WARPS 8
+#endif
+#ifndef IVFTQ_EPI_LD
+#define IVFTQ_EPI_LD 16  // accumulator columns per epilogue TMEM load (16: C2 step 1.17 -> 1.16 ms)
+#endif
+constexpr int kDecWarps = IVFTQ_DEC_WARPS;
+constexpr int kEpiWarp0 = kDecWarp0 + kDecWarps;  // epilogue warps (8)
 constexpr int kEpiWarps = 8;
 constexpr int kSchedWarp = kEpiWarp0 + kEpiWarps;  // 18: item scheduler
 constexpr int kAbWarp0 = kSchedWarp + 1;             // 19..22: A-operand builders
@@ -767,13 +773,17 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const int* ids = (const int*)(mp + Lo.m_ids);
       const int c0 = half * cols;
 #pragma unroll 1
-      for (int cc = 0; cc < cols; cc += 32) {
-        uint32_t r[32];
+      for (int cc = 0; cc < cols; cc += IVFTQ_EPI_LD) {
+        uint32_t r[IVFTQ_EPI_LD];
+#if IVFTQ_EPI_LD == 32
         sm100::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
+#else
+        tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
+#endif
         sm100::tmem_ld_wait();
         ETRACE(cc == 0 ? 0 : 2, clock64());
 #pragma unroll
-        for (int h = 0; h < 32; h += kDrain) {
+        for (int h = 0; h < IVFTQ_EPI_LD; h += kDrain) {
           // the other half's k-th bounds this pair too (either half's K
           // entries are pair candidates); ignore it unless it is this item's
           const unsigned long long o = *(volatile unsigned long long*)&thr_sh[(half ^ 1) * kM + row];
@@ -812,7 +822,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
             *(volatile unsigned long long*)&thr_sh[half * kM + row] =
                 ((unsigned long long)tag << 32) | __float_as_uint(top.kth());
           }
-          if (h + kDrain >= 32) ETRACE(cc == 0 ? 1 : 3, clock64());
+          if (h + kDrain >= IVFTQ_EPI_LD) ETRACE(cc == 0 ? 1 : 3, clock64());
         }
       }
       sm100::tc_fence_before();
