@@ -242,6 +242,8 @@ struct RegTopK {
 constexpr int gcd_c(int a, int b) { return b ? gcd_c(b, a % b) : a; }
 
 constexpr int kTraceTiles = 4096;
+constexpr int kSeedP = 4;  // seed slots per query / 32 (IVFTQ_SEED_P overrides): 128 slots
+                           // (C3 n_p=32: scan 1.46 -> 1.37 ms, 5.32 -> 5.45 M QPS; C2 neutral)
 // Timeline instrumentation (CTA 0, lane 0 of the role's first warp), compiled
 // in only for the trace build (make trace -> libivftq_b200_trace.so, used with
 // IVFTQ_LIB=... and IVFTQ_TRACE=<file>): even untaken, the checks cost ~5 %.
@@ -996,60 +998,79 @@ __global__ void q16_kernel(const float* __restrict__ qrot, int64_t nq, int d, in
 // query's final k-th score is at least their k-th; the margin covers the
 // difference between this f32 arithmetic and the tensor-core scan's
 // (|res| <= ~1 with ~2^-22 relative error each way). One warp per query.
-template <int P>
+template <int P, int FB>
 __global__ void __launch_bounds__(256)
 seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
                   const double* __restrict__ coarse, const float* __restrict__ qrot,
                   const double* __restrict__ levels, int64_t nq, int n_p, int k,
                   long long* __restrict__ key) {
-  __shared__ float t32[256];          // f32 level table (2^(bits+1) <= 256 fields)
-  __shared__ float qs_all[8][kMaxDim];  // each warp's rotated query row
+  constexpr int FPW = 32 / FB;
+  constexpr uint32_t mask = (1u << FB) - 1u;
+  __shared__ float t32[1 << FB];           // f32 level table
+  __shared__ float qs_all[8][kMaxDim + 8];  // each warp's rotated query row (zero-padded)
+  __shared__ double sc_all[8][32 * P];     // each warp's candidate scores
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int fb = st.field_bits, fpw = st.fields_per_word, W = st.words_per_vec;
-  for (int c = threadIdx.x; c < (1 << fb); c += blockDim.x) t32[c] = (float)levels[c];
+  const int W = st.words_per_vec, d = st.dim;
+  for (int c = threadIdx.x; c < (1 << FB); c += blockDim.x) t32[c] = (float)levels[c];
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   float* qr = qs_all[warp];
   if (q < nq)
-    for (int j = lane; j < st.dim; j += 32) qr[j] = qrot[q * st.dim + j];
+    for (int j = lane; j < W * FPW; j += 32) qr[j] = j < d ? qrot[q * d + j] : 0.f;
   __syncthreads();
   if (q >= nq) return;
   const int l0 = probe[q * n_p];
   const int m = min(st.list_size[l0], 32 * P);
-  const uint32_t mask = (1u << fb) - 1u;
   const double cs = coarse[q * n_p];
-  double sc[P];
+  double* scw = sc_all[warp];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    sc[p] = -INFINITY;
+    double v = -INFINITY;
     const int i = p * 32 + lane;
     if (i < m) {
       const int64_t slot = st.list_offset[l0] + i;
       const uint32_t* cw = st.codes + (slot >> 5) * W * 32 + (slot & 31);
-      float acc = 0.f;
-      for (int w0 = 0, j = 0; w0 < W; w0 += 8) {  // 8 words in flight per batch
+      // four partial sums (fields f % 4): independent chains; the f32 result
+      // differs from a sequential fold by a few ulps, inside the bound's margin
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int w0 = 0; w0 < W; w0 += 8) {  // 8 words in flight per batch
         uint32_t wd[8];
 #pragma unroll
         for (int x = 0; x < 8; ++x) wd[x] = w0 + x < W ? cw[(w0 + x) * 32] : 0u;
 #pragma unroll
-        for (int x = 0; x < 8; ++x)
-          for (int f = 0; f < fpw && j < st.dim && w0 + x < W; ++f, ++j)
-            acc = __fadd_rn(acc, __fmul_rn(qr[j], t32[(wd[x] >> (f * fb)) & mask]));
+        for (int x = 0; x < 8; ++x) {
+          if (w0 + x < W) {
+            const float* qw = qr + (w0 + x) * FPW;  // padded past d with zeros
+#pragma unroll
+            for (int f = 0; f < FPW; ++f)
+              acc[f & 3] = __fmaf_rn(qw[f], t32[(wd[x] >> (f * FB)) & mask], acc[f & 3]);
+          }
+        }
       }
+      const float dot = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       const float nrm = __half2float(__ushort_as_half(st.norms[slot]));
-      sc[p] = cs + (double)__fmul_rn(nrm, acc);
+      v = cs + (double)__fmul_rn(nrm, dot);
     }
+    scw[p * 32 + lane] = v;
   }
+  __syncwarp();
   // k-th best: the largest value with at least k values >= it (slots past
-  // the list hold -inf and never qualify)
-  double kth = -INFINITY;
+  // the list hold -inf and never qualify); candidates broadcast from shared
+  double mine[P];
+  int ge[P];
 #pragma unroll
   for (int p = 0; p < P; ++p) {
-    int ge = 0;
-    for (int o = 0; o < 32; ++o)
-#pragma unroll
-      for (int r = 0; r < P; ++r) ge += __shfl_sync(kFull, sc[r], o) >= sc[p];
-    if (ge >= k && sc[p] > -INFINITY) kth = fmax(kth, sc[p]);
+    mine[p] = scw[p * 32 + lane];
+    ge[p] = 0;
   }
+  for (int o = 0; o < 32 * P; ++o) {
+    const double v = scw[o];
+#pragma unroll
+    for (int p = 0; p < P; ++p) ge[p] += v >= mine[p];
+  }
+  double kth = -INFINITY;
+#pragma unroll
+  for (int p = 0; p < P; ++p)
+    if (ge[p] >= k && mine[p] > -INFINITY) kth = fmax(kth, mine[p]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) kth = fmax(kth, __shfl_xor_sync(kFull, kth, o));
   if (lane == 0) {
@@ -1256,17 +1277,24 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
     thr_init_kernel<<<(unsigned)((nq + 255) / 256), 256, 0, side>>>(S.thr_key, nq);
   } else {
     const char* sp_env = getenv("IVFTQ_SEED_P");
-    const int sp = sp_env ? atoi(sp_env) : 1;
+    const int sp = sp_env ? atoi(sp_env) : kSeedP;
     const unsigned sb = (unsigned)((nq + 7) / 8);
-    if (sp >= 4)
-      seed_bound_kernel<4><<<sb, 256, 0, side>>>(*st, probe, coarse, qrot, levels, nq, n_p,
-                                                 depth, S.thr_key);
-    else if (sp == 2)
-      seed_bound_kernel<2><<<sb, 256, 0, side>>>(*st, probe, coarse, qrot, levels, nq, n_p,
-                                                 depth, S.thr_key);
-    else
-      seed_bound_kernel<1><<<sb, 256, 0, side>>>(*st, probe, coarse, qrot, levels, nq, n_p,
-                                                 depth, S.thr_key);
+#define SEED_CASE(PV, FBV)                                                              \
+  seed_bound_kernel<PV, FBV><<<sb, 256, 0, side>>>(*st, probe, coarse, qrot, levels, nq, \
+                                                   n_p, depth, S.thr_key)
+#define SEED_FB(PV)                                                 \
+  if (st->field_bits == 3) SEED_CASE(PV, 3);                        \
+  else if (st->field_bits == 4) SEED_CASE(PV, 4);                   \
+  else SEED_CASE(PV, 5)
+    if (sp >= 4) {
+      SEED_FB(4);
+    } else if (sp == 2) {
+      SEED_FB(2);
+    } else {
+      SEED_FB(1);
+    }
+#undef SEED_FB
+#undef SEED_CASE
   }
   if (int e = check_launch("thr_init")) return e;
   {  // the scan's A-operand rows (fp16 hi/lo of the rotated queries), also off the main stream
