@@ -770,7 +770,10 @@ probe_pick_kernel(const double* __restrict__ X, const double* __restrict__ C, in
 #ifndef IVFTQ_SEL_MINB
 #define IVFTQ_SEL_MINB 8  // 64 registers: C3 select 142 -> 129 us, C2 123 -> 127
 #endif
-constexpr int kSelThreads = 128;
+#ifndef IVFTQ_SEL_THREADS
+#define IVFTQ_SEL_THREADS 128
+#endif
+constexpr int kSelThreads = IVFTQ_SEL_THREADS;
 constexpr int kSelRowCap = 16384;  // lists staged per row (larger L: f64 path)
 
 __host__ __device__ inline size_t sel_region_a(int L) {
@@ -934,7 +937,7 @@ probe_select_kernel(const float* __restrict__ S, const double* __restrict__ X,
       const int k = lane + 32 * m;
       xr[m] = (m < M && k < d) ? xs[k] : 0.0;
     }
-    for (int base = warp * 8; base < nc; base += 4 * 8) {
+    for (int base = warp * 8; base < nc; base += (kSelThreads / 32) * 8) {
       double p[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {

@@ -876,7 +876,10 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
 // and work items are emitted tile-major (every list's first query tile before
 // any second tile). A query's best-ranked lists are therefore scanned first,
 // which tightens its global pruning bound (thr_key) before its far lists run.
-constexpr int kRC = 8;
+#ifndef IVFTQ_RC
+#define IVFTQ_RC 8
+#endif
+constexpr int kRC = IVFTQ_RC;
 
 __global__ void pair_count_kernel(const int32_t* __restrict__ probe, int64_t npairs, int n_p,
                                   int32_t* __restrict__ cnt2) {
