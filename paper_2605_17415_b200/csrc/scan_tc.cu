@@ -774,8 +774,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const float* nsc = (const float*)(mp + Lo.m_nsc);
       const int* ids = (const int*)(mp + Lo.m_ids);
       const int c0 = half * cols;
+      // a warp whose 32 query rows all lie past the item's queries (zero A
+      // rows) has nothing to take: it skips the tile and frees its issue slots
+      const int cols_here = quad * 32 < c.nqt ? cols : 0;
 #pragma unroll 1
-      for (int cc = 0; cc < cols; cc += IVFTQ_EPI_LD) {
+      for (int cc = 0; cc < cols_here; cc += IVFTQ_EPI_LD) {
         uint32_t r[IVFTQ_EPI_LD];
 #if IVFTQ_EPI_LD == 32
         sm100::tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + ab * NV + c0 + cc, r);
