@@ -429,7 +429,8 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": "queries/s",
                     "h2d_bytes_per_step": int(queries.nbytes),
-                    "d2h_bytes_per_step": int(nq * 10 * 16)},
+                    "d2h_bytes_per_step": int(nq * 10 * 16),
+                    "steps_ms": [round(t, 3) for t in e2e_t]},
             "clocks": clk,
             "gpu_launches": int(launches),
             "ingest": {"adds_per_sec_e2e": len(base) / ingest_s,
