@@ -70,11 +70,23 @@ constexpr int kEpiWarps = 8;
 constexpr int kSchedWarp = kEpiWarp0 + kEpiWarps;  // 18: item scheduler
 constexpr int kAbWarp0 = kSchedWarp + 1;             // 19..22: A-operand builders
 constexpr int kThreads = 32 * (kAbWarp0 + 4);        // 736
-constexpr int kItemSlots = 2;    // item-record ring (scheduler -> producer)
+#ifndef IVFTQ_ITEM_SLOTS
+#define IVFTQ_ITEM_SLOTS 2
+#endif
+#ifndef IVFTQ_META
+#define IVFTQ_META 4
+#endif
+constexpr int kItemSlots = IVFTQ_ITEM_SLOTS;  // item-record ring (scheduler -> producer)
 constexpr int kEpiThreads = 32 * kEpiWarps;
 constexpr int kDrain = 16;       // columns per TMEM load / candidate drain
 constexpr int kNS = 4;           // stage ring depth (power of two)
-constexpr int kMeta = 4;         // tile-record ring depth (power of two)
+constexpr int kMeta = IVFTQ_META;  // tile-record ring depth (power of two)
+// mbarrier slots (8 bytes each): st_full[8] st_empty[8] op_full[2] op_empty[2]
+// a_full[2] a_empty[2] meta_full[kMeta] meta_empty[kMeta] it_full[kItemSlots]
+// it_empty[kItemSlots] acc_full[kAccMax] acc_empty[kAccMax]
+constexpr int kBarMetaF = 24, kBarMetaE = kBarMetaF + kMeta, kBarItF = kBarMetaE + kMeta,
+              kBarItE = kBarItF + kItemSlots, kBarAccF = kBarItE + kItemSlots,
+              kBarAccE = kBarAccF + 4, kBarCount = kBarAccE + 4;
 constexpr int kAccMax = 4;       // TMEM accumulator ring depth bound (power of two)
 // Tile shapes (vectors per tile = MMA N, accumulator ring depth): 128 x 2 when
 // shared memory and TMEM allow, else 64 x 4. TMEM budget: nAcc accumulators of
@@ -147,7 +159,7 @@ __host__ __device__ inline Layout make_layout(int NV, int NS, int DP, int W, int
   L.thr = take(2 * kM * 8);  // per half and row: (item tag << 32) | f32 k-th score
   L.item_bytes = align_up(sizeof(ItemRec), 128);
   L.items = take(L.item_bytes * kItemSlots);
-  L.bars = take(8 * 48);
+  L.bars = take(8 * kBarCount);
   L.misc = take(64);
   L.total = off;
   return L;
@@ -339,14 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   uint64_t* st_empty = bars + 8;       // [NS] decoders + epilogue -> producer
   uint64_t* op_full = bars + 16;       // [2] decoders -> MMA
   uint64_t* op_empty = bars + 18;      // [2] MMA commit -> decoders
-  uint64_t* acc_full = bars + 36;      // [nAcc] MMA commit -> epilogue
-  uint64_t* acc_empty = bars + 40;     // [nAcc] epilogue -> MMA
+  uint64_t* acc_full = bars + kBarAccF;   // [nAcc] MMA commit -> epilogue
+  uint64_t* acc_empty = bars + kBarAccE;  // [nAcc] epilogue -> MMA
   uint64_t* a_full = bars + 20;        // [nA] decoders -> MMA (A operand built)
   uint64_t* a_empty = bars + 22;       // [nA] MMA commit -> decoders (A operand free)
-  uint64_t* meta_full = bars + 26;     // [kMeta] decoders -> MMA/epilogue (tile record)
-  uint64_t* meta_empty = bars + 30;    // [kMeta] epilogue -> decoders
-  uint64_t* it_full = bars + 34;       // [kItemSlots] scheduler -> producer
-  uint64_t* it_empty = bars + 44;      // [kItemSlots] producer -> scheduler
+  uint64_t* meta_full = bars + kBarMetaF;   // [kMeta] decoders -> MMA/epilogue (tile record)
+  uint64_t* meta_empty = bars + kBarMetaE;  // [kMeta] epilogue -> decoders
+  uint64_t* it_full = bars + kBarItF;       // [kItemSlots] scheduler -> producer
+  uint64_t* it_empty = bars + kBarItE;      // [kItemSlots] producer -> scheduler
   uint32_t* tmem_slot = (uint32_t*)(smem + Lo.misc);
   for (int i = tid; i < 2 * kM; i += kThreads) ((unsigned long long*)(smem + Lo.thr))[i] = 0ull;
   auto meta = [&](int m) { return smem + Lo.meta0 + (uint32_t)m * Lo.meta_bytes; };
