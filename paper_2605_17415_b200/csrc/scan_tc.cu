@@ -61,6 +61,9 @@ constexpr int kDecWarp0 = 2;     // decoder warps 2..9
 #ifndef IVFTQ_DEC_WARPS
 #define IVFTQ_DEC_WARPS 8
 #endif
+#ifndef IVFTQ_MID_PUBLISH
+#define IVFTQ_MID_PUBLISH 1  // publish the pair K-th to the global bound per tile (C2 n_p=16 scan -1 %)
+#endif
 #ifndef IVFTQ_EPI_LD
 #define IVFTQ_EPI_LD 16  // accumulator columns per epilogue TMEM load (16: C2 step 1.17 -> 1.16 ms)
 #endif
@@ -761,6 +764,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
     RegTopK<KMAX> top;
     top.init();
     double cs = 0.0;
+    uint64_t pub = 0ull;  // last mid-item published K-th key
     uint32_t t = 0, tag = 0;
     const int cols = NV / 2;
     for (;;) {
@@ -781,6 +785,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         top.init();
         tag = t + 1;  // identical in both halves: they consume the same tiles
         cs = pi >= 0 ? P.coarse[pi] : 0.0;  // consumed at the item's end
+        pub = 0ull;
       }
       sm100::tc_fence_after();
       const float* nsc = (const float*)(mp + Lo.m_nsc);
@@ -846,6 +851,16 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&acc_empty[ab]);
       ETRACE(4, clock64());
+#if IVFTQ_MID_PUBLISH
+      // Mid-item bound: once this half holds KMAX >= k candidates of the pair,
+      // their K-th score lower-bounds the query's final k-th, so the global
+      // bound (read per tile by every item of the query) can rise now rather
+      // than at the item's end. Published only when it improved.
+      if (c.tile + 1 < c.ntiles && row < c.nqt && top.k[KMAX - 1] > pub) {
+        pub = top.k[KMAX - 1];
+        atomicMax(&P.thr_key[pi / P.n_p], dkey(cs + (double)key_score(pub)));
+      }
+#endif
       if (c.tile == c.ntiles - 1 && row < c.nqt) {
         // Append this half's candidates of the (query, list) pair to the
         // query's buffer -- only those at or above the query's current global
