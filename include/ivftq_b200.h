@@ -172,6 +172,14 @@ size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists, int dim);
 int ivftq_probe(const double* qn, const float* centroids, int64_t nq, int n_lists,
                 int dim, int n_p, int32_t* probe_out, double* coarse_out,
                 void* scratch, size_t scratch_bytes, void* stream);
+/* The same with the centroids' tensor-core operand images already made by
+ * ivftq_coarse_prepare (ivftq_coarse_prep_bytes(n_lists, dim) bytes) for this
+ * centroid set: a caller that searches one index many times prepares once.
+ * `centroids` is still read by the f64 fallback. */
+int ivftq_probe_prepared(const double* qn, const float* centroids, const void* prepared,
+                         int64_t nq, int n_lists, int dim, int n_p, int32_t* probe_out,
+                         double* coarse_out, void* scratch, size_t scratch_bytes,
+                         void* stream);
 /* List scan + per-query top-`depth` (index.py:441-483): score =
  * coarse + (double)(||r|| * sum_j qrot_j * levels[code_j]). levels: f64
  * flattened reconstruction table (lloydmax.py:146-150). ids are internal. */

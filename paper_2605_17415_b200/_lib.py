@@ -77,6 +77,8 @@ _SIGS = {
     "ivftq_coarse_prep_bytes": (_sz, [_i32, _i32]),
     "ivftq_coarse_prepare": (_i32, [_vp, _i32, _i32, _vp, _vp]),
     "ivftq_probe": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "ivftq_probe_prepared": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz,
+                                    _vp]),
     "ivftq_scan_scratch_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "ivftq_scan_topk": (_i32, [C.POINTER(IvftqStore), _vp, _vp, _vp, _vp, _i64, _i32, _i32,
                                _vp, _vp, _vp, _sz, _vp]),

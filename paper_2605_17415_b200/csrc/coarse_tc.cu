@@ -1135,7 +1135,7 @@ extern "C" size_t ivftq_probe_tc_scratch_bytes(int64_t nq, int n_lists, int dim)
 // Tensor-core probes; returns IVFTQ_ERR_UNSUPPORTED when the caller should use f64.
 int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, int dim,
              int n_p, int32_t* probe_out, double* coarse_out, void* scratch,
-             size_t scratch_bytes, cudaStream_t s) {
+             size_t scratch_bytes, cudaStream_t s, const void* prepared) {
   if (!ivftq_coarse_tc_supported(dim, n_lists) || n_p > 128) return IVFTQ_ERR_UNSUPPORTED;
   if (scratch_bytes < ivftq_probe_tc_scratch_bytes(nq, n_lists, dim)) return IVFTQ_ERR_UNSUPPORTED;
   unsigned char* prep = (unsigned char*)scratch;
@@ -1145,7 +1145,11 @@ int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, 
   int32_t* cand = (int32_t*)(S + (((size_t)nq * n_lists + 63) & ~(size_t)63));
   int32_t* cnt = cand + nq * kCandCap;
   uint32_t* xsplit = (uint32_t*)(((uintptr_t)(cnt + nq) + 255) & ~(uintptr_t)255);
-  if (int e = ivftq_coarse_prepare(centroids, n_lists, dim, prep, s)) return e;
+  if (prepared) {  // operand images made once per centroid set by the caller
+    prep = (unsigned char*)prepared;
+  } else if (int e = ivftq_coarse_prepare(centroids, n_lists, dim, prep, s)) {
+    return e;
+  }
   if (int e = coarse_gemm(qn, nq, dim, n_lists, prep, S, nullptr, nullptr, s, xsplit)) return e;
   const unsigned blocks = (unsigned)((nq + 7) / 8);
   const double* c64 = (const double*)(prep + c64_offset(n_lists, dim));

@@ -570,7 +570,7 @@ extern "C" int ivftq_select_topn(const double* scores, int64_t rows, int cols, i
 extern bool g_probe_tc_force;
 int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, int dim,
              int n_p, int32_t* probe_out, double* coarse_out, void* scratch,
-             size_t scratch_bytes, cudaStream_t s);
+             size_t scratch_bytes, cudaStream_t s, const void* prepared);
 extern "C" size_t ivftq_probe_tc_scratch_bytes(int64_t nq, int n_lists, int dim);
 extern "C" int ivftq_coarse_tc_supported(int dim, int n_lists);
 static bool probe_tc_auto() { return ivftq_coarse_tc_supported(128, 1) != 0; }  // mode != 1
@@ -593,9 +593,28 @@ static size_t probe_f64_scratch_bytes(int64_t nq, int n_lists) {
   return (size_t)nq * n_lists * sizeof(double) + 256;
 }
 
+static int probe_impl(const double* qn, const float* centroids, const void* prepared,
+                      int64_t nq, int n_lists, int dim, int n_p, int32_t* probe_out,
+                      double* coarse_out, void* scratch, size_t scratch_bytes, void* stream);
+
 extern "C" int ivftq_probe(const double* qn, const float* centroids, int64_t nq, int n_lists,
                            int dim, int n_p, int32_t* probe_out, double* coarse_out,
                            void* scratch, size_t scratch_bytes, void* stream) {
+  return probe_impl(qn, centroids, nullptr, nq, n_lists, dim, n_p, probe_out, coarse_out,
+                    scratch, scratch_bytes, stream);
+}
+
+extern "C" int ivftq_probe_prepared(const double* qn, const float* centroids,
+                                    const void* prepared, int64_t nq, int n_lists, int dim,
+                                    int n_p, int32_t* probe_out, double* coarse_out,
+                                    void* scratch, size_t scratch_bytes, void* stream) {
+  return probe_impl(qn, centroids, prepared, nq, n_lists, dim, n_p, probe_out, coarse_out,
+                    scratch, scratch_bytes, stream);
+}
+
+static int probe_impl(const double* qn, const float* centroids, const void* prepared,
+                      int64_t nq, int n_lists, int dim, int n_p, int32_t* probe_out,
+                      double* coarse_out, void* scratch, size_t scratch_bytes, void* stream) {
   if (scratch_bytes < probe_f64_scratch_bytes(nq, n_lists)) {
     set_error("probe: scratch too small");
     return IVFTQ_ERR_SCRATCH;
@@ -617,7 +636,7 @@ extern "C" int ivftq_probe(const double* qn, const float* centroids, int64_t nq,
   // values do not depend on which batch (or chunk) it arrives in.
   if (probe_tc_enabled() || probe_tc_auto()) {
     const int e = probe_tc(qn, centroids, nq, n_lists, dim, n_p, probe_out, coarse_out, scratch,
-                           scratch_bytes, (cudaStream_t)stream);
+                           scratch_bytes, (cudaStream_t)stream, prepared);
     if (e != IVFTQ_ERR_UNSUPPORTED) return e;
   }
   double* S = (double*)scratch;

@@ -626,14 +626,27 @@ class IvfTqIndex:
         with torch.cuda.stream(side):
             self._rotate(qn, nq, qrot)
             rotated.record(side)
-        _lib.check(self._lib.ivftq_probe(qn.data_ptr(), self._cent.data_ptr(), nq, L, d, n_p,
-                                         probe.data_ptr(), coarse.data_ptr(), pscr.data_ptr(),
-                                         pb, s), "probe")
+        _lib.check(self._lib.ivftq_probe_prepared(
+            qn.data_ptr(), self._cent.data_ptr(), self._coarse_prep().data_ptr(), nq, L, d, n_p,
+            probe.data_ptr(), coarse.data_ptr(), pscr.data_ptr(), pb, s), "probe")
         cur.wait_event(rotated)
         ids, scores = self._scan(qn, nq, probe, coarse, n_p, depth, qrot)
         if rerank_depth > 0:
             ids, scores = self._rerank(qn, nq, ids, depth, k)
         return ids, scores, bad, nq
+
+    def _coarse_prep(self):
+        """Tensor-core operand images of the current centroids (made once per
+        centroid set; the probe then skips its three preparation kernels)."""
+        cent = self._cent
+        if getattr(self, "_cprep_for", None) is not cent:
+            L, d = cent.shape
+            buf = torch.empty(self._lib.ivftq_coarse_prep_bytes(L, d), dtype=torch.uint8,
+                              device=self.device)
+            _lib.check(self._lib.ivftq_coarse_prepare(cent.data_ptr(), L, d, buf.data_ptr(),
+                                                      _lib.stream_ptr()), "coarse_prepare")
+            self._cprep, self._cprep_for = buf, cent
+        return self._cprep
 
     def _rotate(self, qn, nq, qrot):
         """Pi q (rotation.py:35-40, index.py:439): f64 product, f32 result."""
