@@ -167,7 +167,9 @@ int ivftq_select_topn(const double* scores, int64_t rows, int cols, int n,
                       int32_t* idx_out, double* val_out, void* stream);
 /* Coarse probes (index.py:436-438): stable top-n_p of qn.C^T. Tensor-core
  * scores + exact f64 re-scoring of the guard band when supported, else the
- * f64 GEMM + select; both return identical probes and f64 coarse values. */
+ * f64 GEMM + select; both return identical probes, and exact f64 coarse
+ * values that differ only in summation order (a few ulps). The path depends
+ * only on the shape (and ivftq_set_coarse_mode), never on the batch size. */
 size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists, int dim);
 int ivftq_probe(const double* qn, const float* centroids, int64_t nq, int n_lists,
                 int dim, int n_p, int32_t* probe_out, double* coarse_out,
