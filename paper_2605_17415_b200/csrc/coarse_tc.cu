@@ -770,6 +770,9 @@ probe_pick_kernel(const double* __restrict__ X, const double* __restrict__ C, in
 #ifndef IVFTQ_SEL_MINB
 #define IVFTQ_SEL_MINB 8  // 64 registers: C3 select 142 -> 129 us, C2 123 -> 127
 #endif
+#ifndef IVFTQ_SUB_SKIP
+#define IVFTQ_SUB_SKIP 48
+#endif
 #ifndef IVFTQ_SEL_THREADS
 #define IVFTQ_SEL_THREADS 128
 #endif
@@ -890,7 +893,13 @@ probe_select_kernel(const float* __restrict__ S, const double* __restrict__ X,
   __syncthreads();
   const int b = s_b;
   float tau = -INFINITY;
-  if (b > 0) {
+  // on long rows a sparse bin b (<= IVFTQ_SUB_SKIP values) is taken whole:
+  // the lower edge of b is the threshold and the second level's pass over
+  // the row is skipped (measured: C3, L = 4096, 132 -> 120 us; at L = 1024
+  // the extra candidates cost more than the pass)
+  const bool refine = b > 0 && (L < 2048 || hist[b] > (unsigned)IVFTQ_SUB_SKIP);
+  if (b > 0 && !refine) tau = -R + (float)b / scale - band(prep) - R * 0x1p-18f;
+  if (refine) {
     for (int i = tid; i < L; i += kSelThreads) {
       const float t = tmap(srow[i]);
       if (bin_of(t) == b)
