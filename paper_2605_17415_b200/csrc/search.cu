@@ -629,8 +629,8 @@ static int probe_impl(const double* qn, const float* centroids, const void* prep
   // fused per-row selection and an exact f64 re-score of ~n_p gathered
   // centroid rows per query; the f64 path a dense DFMA GEMM plus a top-n_p
   // select. Measured on B200 (scripts/probe_mode_bench.py, nq = 10k): L=1024
-  // n_p=64: f64 0.237 ms vs tc 0.171; L=4096 d=96 n_p=32: 0.718 vs 0.250;
-  // n_p=128: 0.850 vs 0.368; d=200 n_p=64: 1.202 vs 0.318 -- so tensor cores
+  // n_p=64: f64 0.243 ms vs tc 0.180; L=4096 d=96 n_p=32: 0.724 vs 0.223;
+  // n_p=128: 0.858 vs 0.356; d=200 n_p=64: 1.206 vs 0.343 -- so tensor cores
   // whenever supported (mode 0 / 2 / IVFTQ_PROBE_TC=1), never (mode 1). The
   // choice never depends on the batch size, so a query's probes and coarse
   // values do not depend on which batch (or chunk) it arrives in.
