@@ -1,20 +1,34 @@
 #!/usr/bin/env python
-"""Benchmark of the B200 IVF-TQ hot path (search QPS at recall@10, list-scan
-roofline, adds/s) on BASELINE.json configs[1] by default.
+"""Benchmark of the B200 IVF-TQ hot path on the north_star target config.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config c2|pr1|c3] [--nprobe P]
+                  [--config c3|c3_hard|c2|pr1|c4] [--nprobe P]
 
-One step = one `search_batch` of the 10k-query batch (k=10) at the headline
-nprobe over the resident index. Every timed step is bracketed by CUDA events
-on the launching stream; L2 is flushed (a 512 MiB write, larger than the
-126 MB L2) before each step, outside the events. N>1 (torchrun): every rank
-holds a replica and searches its own query batch (weak scaling, no data-path
+Default workload: BASELINE.json configs[2] = C3 (10M x 96 unit-normalised
+Gaussian mixture, 4096 lists, b=4 + sign, 10k queries, k=10), headline
+n_p=32 with the {16,32,64,128} sweep beside it. `north_star`'s target is
+stated on this config, and it fits one GPU.
+
+One step = one `search_batch` of the 10k-query batch at the headline n_p
+over the resident index. Every timed step is bracketed by CUDA events on the
+launching stream; L2 is flushed (a 512 MiB write, larger than the 126 MB L2)
+before each step, outside the events.
+
+The line carries a `parity` block measured in the same run against the CPU
+oracle (oracle/ivftq_oracle.py, the reference's algorithm restated): a seeded
+1k-query sample searched by both (ids up to ties, scores within 1e-4
+relative, recall difference) and a 1M-row window of the 10M codes re-encoded
+by the oracle (flip fraction, list ids, binary16 norms).
+
+N>1: launched under torchrun (or `--gpus N` spawns it): every rank holds a
+replica and searches its own query batch (weak scaling, no data-path
 collective); the reported time is the max over ranks.
 
-`--impl reference` times the CPU restatement of the reference path
-(oracle/ivftq_oracle.py; the reference itself is pure Python and is not on the
-GPU box) on the host cores, rank 0 only.
+`--impl reference` times the CPU restatement of the reference path on the
+host cores (rank 0 only): the same workload, the same host k-means
+centroids, the whole 10M rows encoded in 100k-row `add_batch` chunks, then
+`search_batch` on a bounded query sample per step. The reference itself is
+pure Python and is not on the GPU box.
 """
 
 from __future__ import annotations
@@ -32,8 +46,10 @@ import numpy as np
 
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
 
 METRIC = "QPS at recall@10 (nprobe sweep); list-scan HBM GB/s vs peak; adds/sec"
+HEADLINE_NP = {"c3": 32, "c3_hard": 32, "c2": 64, "pr1": 16, "c4": 64}
 
 
 def parse():
@@ -42,13 +58,30 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--bits", type=int, default=None)
     ap.add_argument("--nprobe", type=int, default=None)
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--n", type=int, default=None, help="override database size (testing)")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--parity-queries", type=int, default=1000)
+    ap.add_argument("--parity-rows", type=int, default=1_000_000)
+    ap.add_argument("--ref-step-seconds", type=float, default=2.0)
+    ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` outside torchrun: relaunch this script as N ranks (127.0.0.1)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def peaks():
@@ -60,7 +93,7 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampled every 200 ms while the timed region runs."""
+    """nvidia-smi sampled every 100 ms while the timed region runs."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -75,7 +108,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
                 stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
@@ -108,58 +141,38 @@ def code_bytes(bits: int, d: int) -> int:
     return -(-bits * d // 8) + -(-d // 8) + 2
 
 
-def train_centroids(w, xn_host):
-    from paper_2605_17415_b200.partition import train_partition
-
-    n = len(xn_host)
-    m = w.kmeans_sample or n
-    rng = np.random.default_rng(w.base_seed + 17)
-    sub = xn_host[np.sort(rng.choice(n, size=min(m, n), replace=False))] if m < n else xn_host
-    return train_partition(sub, w.n_lists, seed=42, max_iters=w.kmeans_iters).centroids
-
-
-def setup(args, rank):
+def workload(args, query_offset: int = 0):
     from paper_2605_17415_b200.workloads import make_workload
 
-    w = make_workload(args.config)
+    over = {}
     if args.n:
-        w = make_workload(args.config, n=args.n)
+        over["n"] = args.n
+    if args.bits:
+        over["bits"] = args.bits
+    w = make_workload(args.config, **over)
+    if query_offset:
+        w = make_workload(args.config, query_seed=w.query_seed + query_offset, **over)
     nq = args.nq or w.n_queries
-    base = w.base()
-    queries = make_workload(args.config, query_seed=w.query_seed + rank).queries(nq)
-    xn = base.astype(np.float64)
-    xn /= np.linalg.norm(xn, axis=1)[:, None]
-    n_p = args.nprobe or max(w.nprobe)
-    return w, base, xn, queries, nq, n_p
+    n_p = args.nprobe or HEADLINE_NP.get(w.name, max(w.nprobe))
+    return w, nq, n_p
 
 
-def cpu_oracle_index(idx):
-    """Oracle index holding the GPU-encoded fields (bit-identical to its own encode)."""
-    from oracle import ivftq_oracle as orc
-
-    o = orc.OracleIndex(idx.partition.centroids, idx.rot.matrix, idx.quantizer.boundaries,
-                        idx.quantizer.centroids, idx.quantizer.half_bin_means,
-                        use_sign=idx.config.use_sign_bit)
-    o.bins, o.signs = idx.bins, idx.signs
-    o.list_ids, o.norms = idx.list_ids, idx.norms
-    return o
+def kmeans_sample(w, base):
+    """Seeded subsample for host k-means, unit rows in f64."""
+    n = len(base)
+    m = min(w.kmeans_sample or n, n)
+    rng = np.random.default_rng(w.base_seed + 17)
+    sub = base[np.sort(rng.choice(n, size=m, replace=False))] if m < n else base
+    sub = sub.astype(np.float64)
+    return sub / np.linalg.norm(sub, axis=1)[:, None]
 
 
-def time_cpu_search(o, queries, k, n_p, seconds):
-    """Reference protocol (harness.py:281-289): 8-query warm-up, then perf_counter."""
-    o.search_batch(queries[:8], k, n_p)
-    m = 16
-    t0 = time.perf_counter()
-    o.search_batch(queries[:m], k, n_p)
-    rate = m / (time.perf_counter() - t0)
-    m = int(min(len(queries), max(16, rate * seconds)))
-    t0 = time.perf_counter()
-    o.search_batch(queries[:m], k, n_p)
-    dt = time.perf_counter() - t0
-    return m / dt, m, dt
+# ----------------------------------------------------------------------------
+# reference arm
 
 
 def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -167,8 +180,13 @@ def run_reference(args):
     from paper_2605_17415_b200.quantizer import design_quantizer
     from paper_2605_17415_b200.rotation import generate_rotation
 
-    w, base, xn, queries, nq, n_p = setup(args, 0)
-    cent = train_centroids(w, xn)
+    w, nq, n_p = workload(args)
+    base = w.base()
+    queries = w.queries(nq)
+    t0 = time.perf_counter()
+    cent = orc.train_partition(kmeans_sample(w, base), w.n_lists, seed=42,
+                               max_iters=w.kmeans_iters)
+    kmeans_s = time.perf_counter() - t0
     q = design_quantizer(w.bits, w.d)
     R = generate_rotation(w.d, 42)
     o = orc.OracleIndex(cent, R.matrix, q.boundaries, q.centroids, q.half_bin_means)
@@ -176,11 +194,12 @@ def run_reference(args):
     for s in range(0, len(base), 100_000):  # 100k-row add_batch chunks
         o.add_batch(base[s:s + 100_000])
     adds = len(base) / (time.perf_counter() - t0)
-    o.search_batch(queries[:8], 10, n_p)
+    o.scoring_rows()  # the reference caches W across searches (index.py:366-378)
+    o.search_batch(queries[:8], 10, n_p)  # 8-query warm-up (harness.py:281-289)
     t0 = time.perf_counter()
     o.search_batch(queries[:16], 10, n_p)
     rate = 16 / (time.perf_counter() - t0)
-    per_step = int(min(nq, max(8, rate * 6.0)))
+    per_step = int(min(nq, max(8, rate * args.ref_step_seconds)))
     for i in range(args.warmup):
         o.search_batch(queries[:per_step], 10, n_p)
     times = []
@@ -193,20 +212,94 @@ def run_reference(args):
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": METRIC, "value": qps, "unit": "queries/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000 * float(np.mean(times)), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+        "data": "synthetic (seeded Gaussian mixture, SURVEY §8d)",
         "config": {"workload": w.name, "n": len(base), "d": w.d, "n_lists": w.n_lists,
-                   "bits": w.bits, "k": 10, "nprobe": n_p, "nq_per_step": per_step},
+                   "bits": w.bits, "sign_bit": True, "nq": nq, "k": 10, "nprobe": n_p,
+                   "kmeans": f"host f64 k-means++/Lloyd on a seeded {w.kmeans_sample}-row "
+                             f"subsample, {w.kmeans_iters} iters (same centroids as ours)",
+                   "nq_per_step": per_step},
         "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": cores, "kind": "port",
                          "sample": f"{per_step} queries per step of the {nq}-query batch; "
                                    f"oracle restatement of the reference (numpy/OpenBLAS, "
-                                   f"all {cores} threads)"},
+                                   f"all {cores} threads), single process like the reference"},
         "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
         "ingest": {"adds_per_sec": adds, "rows": len(base), "chunk": 100_000},
+        "setup_s": {"kmeans": round(kmeans_s, 1)},
     }
     print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# our arm
+
+
+def parity_block(idx, base, queries, cent, R, q, ids_gpu, sc_gpu, truth, n_p, args):
+    """Oracle parity on bounded samples of the benchmarked index (rank 0)."""
+    from oracle import ivftq_oracle as orc
+    from helpers import compare_topk
+    from paper_2605_17415_b200.evaluation import recall_at_k
+
+    out = {}
+    # ---- codes: a contiguous 1M-row window re-encoded by the oracle ----------
+    t0 = time.perf_counter()
+    n = len(base)
+    pr = min(args.parity_rows, n)
+    off = int(np.random.default_rng(7).integers(0, n - pr + 1))
+    bins, signs, lids, nrm = idx.bins, idx.signs, idx.list_ids, idx.norms
+    flips = 0
+    vec_flips = 0
+    lid_eq = True
+    nrm_eq = True
+    for s in range(off, off + pr, 100_000):
+        e = min(off + pr, s + 100_000)
+        b_o, s_o, l_o, n_o, _ = orc.encode_batch(base[s:e], cent, R.matrix, q.boundaries,
+                                                 q.centroids)
+        bad = (bins[s:e] != b_o) | (signs[s:e] != s_o)
+        flips += int(bad.sum())
+        vec_flips += int(bad.any(axis=1).sum())
+        lid_eq &= bool(np.array_equal(lids[s:e], l_o))
+        nrm_eq &= bool(np.array_equal(nrm[s:e].view(np.uint16), n_o.view(np.uint16)))
+    out["codes"] = {"rows": pr, "offset": off, "flip_fraction": flips / (pr * base.shape[1]),
+                    "vectors_with_flips": vec_flips, "list_ids_equal": lid_eq,
+                    "norms_equal": nrm_eq, "s": round(time.perf_counter() - t0, 1)}
+    # ---- search: a seeded query sample through the oracle over the same codes -
+    t0 = time.perf_counter()
+    o = orc.OracleIndex(cent, R.matrix, q.boundaries, q.centroids, q.half_bin_means)
+    o.bins, o.signs, o.list_ids, o.norms = bins, signs, lids, nrm
+    o.scoring_rows()
+    nq = len(queries)
+    pq = min(args.parity_queries, nq)
+    sel = np.sort(np.random.default_rng(11).choice(nq, size=pq, replace=False))
+    o.search_batch(queries[sel[:8]], 10, n_p)  # warm-up (harness.py:281-289)
+    t1 = time.perf_counter()
+    oi, os_ = o.search_batch(queries[sel], 10, n_p)
+    cpu_t = time.perf_counter() - t1
+    gi, gs = ids_gpu[sel], sc_gpu[sel]
+    ent = {"nprobe": n_p, "queries": pq, "query_seed": 11}
+    try:
+        ent["queries_differing"] = int(compare_topk(gi, gs, oi, os_))
+        ent["ids_scores_ok"] = True
+    except AssertionError as e:  # recorded, not hidden
+        ent["ids_scores_ok"] = False
+        ent["error"] = str(e)[:300]
+    fin = np.isfinite(os_)
+    ent["max_rel_score_diff"] = float(np.max(np.abs(gs[fin] - os_[fin]) /
+                                             np.maximum(np.abs(os_[fin]), 1e-12)))
+    ent["recall_gpu"] = recall_at_k(gi, truth[sel], 10)
+    ent["recall_oracle"] = recall_at_k(oi, truth[sel], 10)
+    ent["recall_delta_pp"] = 100 * abs(ent["recall_gpu"] - ent["recall_oracle"])
+    ent["s"] = round(time.perf_counter() - t0, 1)
+    out["search"] = ent
+    out["ok"] = bool(ent["ids_scores_ok"] and ent["recall_delta_pp"] <= 0.1 and lid_eq
+                     and nrm_eq and out["codes"]["flip_fraction"] <= 1e-4)
+    out["tolerances"] = ("ids identical up to ties within 1e-4 rel; scores |d| <= 1e-4|s| + "
+                         "1e-6; recall delta <= 0.1 pp; code flips <= 1e-4; list ids and "
+                         "binary16 norms bit-exact")
+    return out, (pq / cpu_t, pq, cpu_t)
 
 
 def run_ours(args):
@@ -224,39 +317,41 @@ def run_ours(args):
     from paper_2605_17415_b200 import _lib
     from paper_2605_17415_b200.evaluation import exact_topk, recall_at_k
     from paper_2605_17415_b200.index import IndexConfig, IvfTqIndex
-    from paper_2605_17415_b200.partition import CoarsePartition
+    from paper_2605_17415_b200.partition import CoarsePartition, train_partition
     from paper_2605_17415_b200.quantizer import design_quantizer
+    from paper_2605_17415_b200.replicas import job_throughput, max_over_ranks, share_centroids
     from paper_2605_17415_b200.rotation import generate_rotation
 
-    from paper_2605_17415_b200.replicas import job_throughput, max_over_ranks, share_centroids
-
     L = _lib.lib()
-    w, base, xn, queries, nq, n_p = setup(args, rank)
-    cent = share_centroids(train_centroids(w, xn) if rank == 0 else None, (w.n_lists, w.d), dev)
+    T = {}
+    t0 = time.perf_counter()
+    w, nq, n_p = workload(args, query_offset=rank)
+    base = w.base()
+    queries = w.queries(nq)
+    T["generate"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    cent_host = (train_partition(kmeans_sample(w, base), w.n_lists, seed=42,
+                                 max_iters=w.kmeans_iters).centroids if rank == 0 else None)
+    cent = share_centroids(cent_host, (w.n_lists, w.d), dev)
+    T["kmeans"] = time.perf_counter() - t0
+    qz = design_quantizer(w.bits, w.d)
+    R = generate_rotation(w.d, 42)
     cfg = IndexConfig(dim=w.d, bits=w.bits, n_lists=w.n_lists)
-    idx = IvfTqIndex(cfg, design_quantizer(w.bits, w.d), generate_rotation(w.d, 42),
-                     CoarsePartition(w.n_lists, w.d, cent), device=dev)
 
-    # ---- ingest: adds/s end to end (host f32 rows -> device lists) ----------
-    chunk = len(base)  # one add_batch of the whole pinned batch (sub-chunked copy/encode overlap inside)
+    def new_index():
+        return IvfTqIndex(cfg, qz, R, CoarsePartition(w.n_lists, w.d, cent), device=dev)
+
+    # ---- ingest: adds/s end to end (pinned host f32 rows -> device lists) ----
+    chunk = 1_000_000
     pinned = torch.from_numpy(base).pin_memory()
-    # warm-up on a throwaway index: first-use allocations and kernel loads stay
-    # out of the timed region (the timed run still grows its own store)
-    warm = IvfTqIndex(cfg, design_quantizer(w.bits, w.d), generate_rotation(w.d, 42),
-                      CoarsePartition(w.n_lists, w.d, cent), device=dev)
-    warm.add_batch(pinned[: min(chunk, 600_000)])
+    warm = new_index()  # first-use allocations and kernel loads stay untimed
+    warm.add_batch(pinned[: min(len(base), 600_000)])
     del warm
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # three timed ingests of the whole batch into fresh indexes (the last one
-    # is the searched index); the median is reported
     ing = []
-    for r in range(3):
-        if r < 2:
-            tgt = IvfTqIndex(cfg, design_quantizer(w.bits, w.d), generate_rotation(w.d, 42),
-                             CoarsePartition(w.n_lists, w.d, cent), device=dev)
-        else:
-            tgt = idx
+    for r in range(3):  # three timed ingests into fresh indexes; the last is searched
+        tgt = new_index()
         torch.cuda.synchronize()
         e0.record()
         for s in range(0, len(base), chunk):
@@ -264,9 +359,9 @@ def run_ours(args):
         e1.record()
         torch.cuda.synchronize()
         ing.append(e0.elapsed_time(e1) / 1000)
+        idx = tgt
         del tgt
     ingest_s = float(np.median(ing))
-    # kernel-only encode throughput on a device-resident chunk
     xd = torch.from_numpy(base[:250_000]).to(dev)
     idx._encode_device(xd)
     torch.cuda.synchronize()
@@ -275,12 +370,25 @@ def run_ours(args):
     e1.record()
     torch.cuda.synchronize()
     enc_s = e0.elapsed_time(e1) / 1000
+    del xd
+    sizes = idx._store.sizes
 
-    # ---- ground truth (GPU brute force, reference tie rule) ----------------
+    # ---- ground truth: f64 brute force on the GPU (reference tie rule) -------
+    t0 = time.perf_counter()
+    xn = torch.empty((len(base), w.d), dtype=torch.float64, device=dev)
+    bad = torch.empty(1, dtype=torch.int64, device=dev)
+    for s in range(0, len(base), chunk):
+        e = min(len(base), s + chunk)
+        xc = pinned[s:e].to(dev)
+        _lib.check(L.ivftq_normalize_rows(xc.data_ptr(), _lib.IVFTQ_F32, e - s, w.d,
+                                          xn[s:e].data_ptr(), bad.data_ptr(),
+                                          _lib.stream_ptr()), "normalize")
     qn = queries.astype(np.float64)
     qn /= np.linalg.norm(qn, axis=1)[:, None]
-    truth = exact_topk(torch.from_numpy(xn).to(dev), qn, 10).ids
-    del xd
+    truth = exact_topk(xn, qn, 10).ids
+    del xn, pinned
+    torch.cuda.empty_cache()
+    T["truth"] = time.perf_counter() - t0
 
     Qd = torch.from_numpy(queries).to(dev)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
@@ -288,20 +396,35 @@ def run_ours(args):
     def step(np_):
         return idx.search_batch(Qd, 10, np_, return_device=True)
 
+    def timed(fn, reps):
+        ts = []
+        for _ in range(reps):
+            flush.fill_(1)
+            torch.cuda.synchronize()
+            e0.record()
+            out = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1000)
+        return ts, out
+
+    # ---- n_p sweep ------------------------------------------------------------
     sweep = []
     for p in w.nprobe:
         step(p)
+        ts, (ids, _) = timed(lambda: step(p), 3)
+        t = float(np.median(ts))
+        ent = {"nprobe": p, "qps": nq / t, "ms": t * 1000,
+               "recall_at_10": recall_at_k(ids.cpu().numpy(), truth, 10)}
+        L.ivftq_set_kernel_timing(1)
         flush.fill_(1)
+        step(p)
         torch.cuda.synchronize()
-        e0.record()
-        ids, _ = step(p)
-        e1.record()
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) / 1000
-        sweep.append({"nprobe": p, "qps": nq / t,
-                      "recall_at_10": recall_at_k(ids.cpu().numpy(), truth, 10)})
+        ent["scan_kernel_ms"] = L.ivftq_last_scan_kernel_ms()
+        L.ivftq_set_kernel_timing(0)
+        sweep.append(ent)
 
-    # ---- headline: K timed steps (device-resident queries) ------------------
+    # ---- headline: K timed steps (device-resident queries) --------------------
     for _ in range(args.warmup):
         step(n_p)
     clocks = Clocks(local)
@@ -322,66 +445,41 @@ def run_ours(args):
         launches += L.ivftq_launch_count() - c0
         times.append(e0.elapsed_time(e1))
     clk = clocks.stop()
+    if world > 1:
+        dist.barrier()
     ms_max = max_over_ranks(float(np.mean(times)), dev)
     value = job_throughput(nq, ms_max)
-    recall = recall_at_k(ids.cpu().numpy(), truth, 10)
+    ids_h, sc_h = ids.cpu().numpy(), sc.cpu().numpy()
+    recall = recall_at_k(ids_h, truth, 10)
 
-    # ---- e2e through the public API with host buffers -----------------------
+    # ---- e2e through the public API with pinned host buffers ------------------
     qpin = torch.from_numpy(queries).pin_memory()
     for _ in range(max(args.warmup, 3)):  # also warms the pinned result buffers
-        hi, hs = idx.search_batch(qpin, 10, n_p)
+        idx.search_batch(qpin, 10, n_p)
     e2e_t = []
     for _ in range(args.steps):
         flush.fill_(1)
         torch.cuda.synchronize()
         e0.record()
-        hi, hs = idx.search_batch(qpin, 10, n_p)  # numpy results (D2H inside)
+        idx.search_batch(qpin, 10, n_p)  # H2D of the queries, numpy ids+scores back
         e1.record()
         torch.cuda.synchronize()
         e2e_t.append(e0.elapsed_time(e1))
     e2e_val = job_throughput(nq, max_over_ranks(float(np.mean(e2e_t)), dev))
 
-    # ---- roofline of the dominant kernel (list scan) ------------------------
-    import ctypes as C
-
-    qnd, bad, _ = idx._normalize_queries_device(Qd)
-    probe = torch.empty((nq, n_p), dtype=torch.int32, device=dev)
-    coarse = torch.empty((nq, n_p), dtype=torch.float64, device=dev)
-    pb = L.ivftq_probe_scratch_bytes(nq, w.n_lists, w.d)
-    pscr = torch.empty(pb, dtype=torch.uint8, device=dev)
-    s = _lib.stream_ptr()
-    _lib.check(L.ivftq_probe(qnd.data_ptr(), idx._cent.data_ptr(), nq, w.n_lists, w.d, n_p,
-                             probe.data_ptr(), coarse.data_ptr(), pscr.data_ptr(), pb, s))
-    qrot = torch.empty((nq, w.d), dtype=torch.float32, device=dev)
-    _lib.check(L.ivftq_gemm_nt(qnd.data_ptr(), idx._R.data_ptr(), 1, nq, w.d, w.d,
-                               qrot.data_ptr(), 0, s))
-    oid = torch.empty((nq, 10), dtype=torch.int64, device=dev)
-    osc = torch.empty((nq, 10), dtype=torch.float64, device=dev)
-    sb = L.ivftq_scan_scratch_bytes(nq, n_p, 10, w.n_lists)
-    sscr = torch.empty(sb, dtype=torch.uint8, device=dev)
-    st = idx._store.struct()
-
-    def scan():
-        _lib.check(L.ivftq_scan_topk(C.byref(st), probe.data_ptr(), coarse.data_ptr(),
-                                     qrot.data_ptr(), idx._levels.data_ptr(), nq, n_p, 10,
-                                     oid.data_ptr(), osc.data_ptr(), sscr.data_ptr(), sb, s))
-
-    scan()
-    sc_t, k_t = [], []
+    # ---- roofline of the dominant kernel (list scan), timed in this run -------
+    k_t = []
     L.ivftq_set_kernel_timing(1)
     for _ in range(max(3, args.steps)):
         flush.fill_(1)
         torch.cuda.synchronize()
-        e0.record()
-        scan()
-        e1.record()
+        step(n_p)
         torch.cuda.synchronize()
-        sc_t.append(e0.elapsed_time(e1) / 1000)
         k_t.append(L.ivftq_last_scan_kernel_ms() / 1000)
     L.ivftq_set_kernel_timing(0)
-    t_scan = float(np.mean(sc_t))       # regroup + scan kernel + per-query merge
-    t_kernel = float(np.mean(k_t))      # the tensor-core scan kernel alone
-    sizes = idx._store.sizes
+    t_kernel = float(np.median(k_t))
+    qnd, _, _ = idx._normalize_queries_device(Qd)
+    probe, _ = idx._probe(qnd, nq, n_p)
     vq = float(sizes[probe.cpu().numpy()].sum())  # sum_q V_q (candidate vectors)
     s_vec = code_bytes(w.bits, w.d)
     alg_bytes = vq * s_vec
@@ -392,14 +490,21 @@ def run_ours(args):
     prof = ROOT / "profiles" / "scan_traffic.json"
     if prof.exists():
         traffic = json.loads(prof.read_text()).get(w.name)
+    store_bytes = int(idx._store.nbytes())
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        o = cpu_oracle_index(idx)
-        qps_cpu, m, dt = time_cpu_search(o, queries, 10, n_p, args.cpu_seconds)
-        cpu = {"value": qps_cpu, "unit": "queries/s", "cores": os.cpu_count(), "kind": "port",
-               "sample": f"{m} of {nq} queries at nprobe={n_p} ({dt:.1f} s), oracle "
-                         f"restatement over the same encoded index, numpy/OpenBLAS all threads"}
+    # ---- parity vs the oracle, CPU baseline (rank 0, N=1) --------------------
+    par, cpu = None, None
+    if rank == 0 and not args.no_parity:
+        t0 = time.perf_counter()
+        par, (qps_cpu, m, dt) = parity_block(idx, base, queries, cent, R, qz, ids_h, sc_h,
+                                             truth, n_p, args)
+        T["parity"] = time.perf_counter() - t0
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = {"value": qps_cpu, "unit": "queries/s", "cores": os.cpu_count(),
+                   "kind": "port",
+                   "sample": f"the parity sample: {m} of {nq} queries at nprobe={n_p} "
+                             f"({dt:.1f} s), oracle restatement over the same encoded "
+                             f"index, numpy/OpenBLAS all threads"}
 
     if rank == 0:
         line = {
@@ -409,21 +514,27 @@ def run_ours(args):
             "dtype": "f32/f64", "data": "synthetic (seeded Gaussian mixture, SURVEY §8d)",
             "config": {"workload": w.name, "n": len(base), "d": w.d, "n_lists": w.n_lists,
                        "bits": w.bits, "sign_bit": True, "nq": nq, "k": 10, "nprobe": n_p,
+                       "components": w.components, "sigma": w.sigma,
+                       "seeds": {"base": w.base_seed, "query": w.query_seed + rank},
+                       "kmeans": f"host f64 k-means++/Lloyd on a seeded {w.kmeans_sample}-row "
+                                 f"subsample, {w.kmeans_iters} iters (same centroids as the "
+                                 f"reference arm)",
                        "parallelism": f"replica x{world} (query-sharded)",
                        "l2": "flushed before every timed step (512 MiB write)"},
             "recall_at_10": recall,
             "sweep": sweep,
-            # The list-major scan re-uses each list's codes for every query probing
-            # it, so it is not HBM-bound: its roofline is the tensor pipe
-            # (algorithmic 2*d flops per (query, candidate); executed MMA work is
-            # 3x that for the fp16 hi/lo split). effective_gbs is the per-query
-            # code stream a query-major scan would read (sum_q V_q * s(b,d)).
+            "parity": par,
+            # The list-major scan reuses each list's codes for every query that
+            # probes it, so it is not HBM-bound: its roofline is the tensor pipe
+            # (algorithmic 2*d flops per (query, candidate); the executed MMA
+            # work is 3x that for the fp16 hi/lo split). effective_gbs is the
+            # per-query code stream a query-major scan would read.
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / tf, "traffic": traffic,
                          "kernel": "scan_tc_kernel", "peak_source": src + " bf16 dense",
                          "alg_flops_per_launch": alg_flops, "kernel_ms": t_kernel * 1000,
-                         "scan_call_ms": t_scan * 1000, "alg_bytes_per_launch": alg_bytes,
-                         "bytes_per_vector": s_vec,
+                         "pairs_per_launch": vq, "alg_bytes_per_launch": alg_bytes,
+                         "bytes_per_vector": s_vec, "store_bytes": store_bytes,
                          "effective_gbs": alg_bytes / t_kernel / 1e9,
                          "effective_frac_of_hbm": alg_bytes / t_kernel / 1e9 / hbm},
             "cpu_baseline": cpu,
@@ -435,7 +546,11 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "ingest": {"adds_per_sec_e2e": len(base) / ingest_s,
                        "adds_per_sec_device_encode": 250_000 / enc_s, "rows": len(base),
-                       "chunk": chunk, "reps_ms": [round(t * 1000, 2) for t in ing], "stat": "median"},
+                       "chunk": chunk, "reps_ms": [round(t * 1000, 2) for t in ing],
+                       "stat": "median"},
+            "list_sizes": {"min": int(sizes.min()), "mean": float(sizes.mean()),
+                           "max": int(sizes.max())},
+            "setup_s": {k: round(v, 1) for k, v in T.items()},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -445,6 +560,8 @@ def run_ours(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     if args.impl == "reference":
         run_reference(args)
     else:

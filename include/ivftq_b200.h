@@ -13,7 +13,14 @@
  *     passed as void*, NULL = legacy default stream);
  *   - return value 0 = success, < 0 = an IVFTQ_ERR_* code; the message is in
  *     ivftq_last_error() (thread-local);
- *   - no global mutable state: concurrent calls on different streams are safe.
+ *   - concurrency: calls from different host threads, on different streams
+ *     or different devices, are independent. The library's only internal
+ *     state is per device (SM count, shared-memory opt-ins; mutex-guarded)
+ *     or per (host thread, device) (the side stream and fork/join events a
+ *     scan uses internally, the kernel-timing events). Internal forks are
+ *     joined back into the caller's stream on every return path, so a call
+ *     inside a stream capture never leaves the capture forked. Process-wide
+ *     switches: ivftq_set_coarse_mode (configuration, atomic).
  */
 #ifndef IVFTQ_B200_H
 #define IVFTQ_B200_H
@@ -103,11 +110,11 @@ int ivftq_assign_tc(const double* xn, const float* centroids, int64_t n, int n_l
                     int dim, int32_t* list_out, void* scratch, size_t scratch_bytes,
                     void* stream);
 /* Coarse-scoring path selection (results are identical in every mode):
- * 0 = default: assignment on tensor cores with the f64 guard band (dim <= 256),
- *     probes on tensor cores when n_lists >= 32 * n_p, else the f64 GEMM +
- *     exact select (the faster of the two on B200);
+ * 0 = default: assignment and probes on tensor cores with the exact f64 guard
+ *     band whenever the shape is supported (padded dim <= 256, n_p <= 128),
+ *     else the f64 GEMM + exact select;
  * 1 = f64 CUDA-core GEMMs only (parity reference);
- * 2 = tensor cores for probes as well (also IVFTQ_PROBE_TC=1). */
+ * 2 = same as 0 (kept for ABI compatibility; also IVFTQ_PROBE_TC=1). */
 int ivftq_set_coarse_mode(int mode);
 int ivftq_coarse_tc_supported(int dim, int n_lists);
 /* Pre-split centroid operand images for the tensor-core coarse GEMM. */

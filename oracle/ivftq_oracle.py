@@ -140,6 +140,35 @@ def unpack_fields(packed: np.ndarray, width: int, count: int) -> np.ndarray:
     return (stream.astype(np.uint16) << np.arange(width)).sum(axis=2).astype(np.uint8)
 
 
+class _Rows:
+    """Append-only rows with capacity doubling (index.py:130-159)."""
+
+    def __init__(self, tail, dtype):
+        self._buf = np.zeros((16,) + tuple(tail), dtype)
+        self._n = 0
+
+    @property
+    def data(self) -> np.ndarray:
+        return self._buf[: self._n]
+
+    def extend(self, rows) -> None:
+        rows = np.asarray(rows, dtype=self._buf.dtype)
+        need = self._n + len(rows)
+        if need > len(self._buf):
+            cap = len(self._buf)
+            while cap < need:
+                cap *= 2
+            nb = np.zeros((cap,) + self._buf.shape[1:], self._buf.dtype)
+            nb[: self._n] = self._buf[: self._n]
+            self._buf = nb
+        self._buf[self._n: need] = rows
+        self._n = need
+
+    def replace(self, rows) -> None:
+        self._buf = np.asarray(rows, dtype=self._buf.dtype)
+        self._n = len(self._buf)
+
+
 class OracleIndex:
     """Stored fields of an index plus the reference's search semantics.
 
@@ -158,12 +187,27 @@ class OracleIndex:
         self.flat = flat
         self.n_lists = len(self.centroids)
         d = self.R.shape[0]
-        self.bins = np.zeros((0, d), np.uint8)
-        self.signs = np.zeros((0, d), np.uint8)
-        self.list_ids = np.zeros(0, np.int64)
-        self.norms = np.zeros(0, np.float16)
-        self.raw = np.zeros((0, d), np.float32) if keep_raw else None
+        # append-only row stores with doubling growth, like the reference's
+        # _Rows (index.py:130-159): add_batch is amortised O(rows added)
+        self._rows = {"bins": _Rows((d,), np.uint8), "signs": _Rows((d,), np.uint8),
+                      "list_ids": _Rows((), np.int64), "norms": _Rows((), np.float16)}
+        if keep_raw:
+            self._rows["raw"] = _Rows((d,), np.float32)
         self._w = None
+
+    bins = property(lambda self: self._rows["bins"].data,
+                    lambda self, v: self._rows["bins"].replace(v))
+    signs = property(lambda self: self._rows["signs"].data,
+                     lambda self, v: self._rows["signs"].replace(v))
+    list_ids = property(lambda self: self._rows["list_ids"].data,
+                        lambda self, v: self._rows["list_ids"].replace(v))
+    norms = property(lambda self: self._rows["norms"].data,
+                     lambda self, v: self._rows["norms"].replace(v))
+
+    @property
+    def raw(self):
+        r = self._rows.get("raw")
+        return None if r is None else r.data
 
     @property
     def count(self) -> int:
@@ -174,12 +218,12 @@ class OracleIndex:
         b, s, l, nr, xn = encode_batch(x, self.centroids, self.R, self.boundaries,
                                        self.qcent, self.flat)
         first = self.count
-        self.bins = np.concatenate([self.bins, b])
-        self.signs = np.concatenate([self.signs, s])
-        self.list_ids = np.concatenate([self.list_ids, l])
-        self.norms = np.concatenate([self.norms, nr])
-        if self.raw is not None:
-            self.raw = np.concatenate([self.raw, xn.astype(np.float32)])
+        self._rows["bins"].extend(b)
+        self._rows["signs"].extend(s)
+        self._rows["list_ids"].extend(l)
+        self._rows["norms"].extend(nr)
+        if "raw" in self._rows:
+            self._rows["raw"].extend(xn.astype(np.float32))
         self._w = None
         return np.arange(first, first + len(l), dtype=np.int64)
 

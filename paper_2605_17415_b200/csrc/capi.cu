@@ -2,6 +2,9 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "common.cuh"
 
@@ -25,6 +28,73 @@ int check_launch(const char* what) {
     return IVFTQ_ERR_CUDA;
   }
   return IVFTQ_OK;
+}
+
+// ---- per-device state ----------------------------------------------------------
+static std::mutex g_dev_mu;
+static std::map<int, int> g_sms;                               // device -> SM count
+static std::map<std::pair<int, const void*>, size_t> g_opted;  // (device, kernel) -> bytes
+
+static int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
+int device_sm_count() {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  auto it = g_sms.find(dev);
+  if (it != g_sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1)
+    n = 148;
+  g_sms[dev] = n;
+  return n;
+}
+
+int smem_opt_in_dev(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return 0;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  size_t& have = g_opted[std::make_pair(dev, fn)];
+  if (bytes <= have) return 0;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    set_error("shared memory request %zu B rejected: %s", bytes, cudaGetErrorString(e));
+    return IVFTQ_ERR_UNSUPPORTED;
+  }
+  have = bytes;
+  return 0;
+}
+
+// One side stream + fork/join events per (host thread, device). Thread-local:
+// never shared between threads, so a capture in one thread cannot absorb
+// another thread's work; released with the thread.
+struct SideStreams {
+  std::map<int, SideStream> by_dev;
+  ~SideStreams() {
+    for (auto& kv : by_dev) {
+      cudaStreamDestroy(kv.second.stream);
+      cudaEventDestroy(kv.second.fork);
+      cudaEventDestroy(kv.second.join);
+    }
+  }
+};
+static thread_local SideStreams t_side;
+
+int side_stream(SideStream** out) {
+  const int dev = current_device();
+  auto it = t_side.by_dev.find(dev);
+  if (it == t_side.by_dev.end()) {
+    SideStream ss{};
+    IVFTQ_CHECK_CUDA(cudaStreamCreateWithFlags(&ss.stream, cudaStreamNonBlocking));
+    IVFTQ_CHECK_CUDA(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    IVFTQ_CHECK_CUDA(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+    it = t_side.by_dev.emplace(dev, ss).first;
+  }
+  *out = &it->second;
+  return 0;
 }
 
 // host mirror of pw_sumsq (same association order, no FMA)

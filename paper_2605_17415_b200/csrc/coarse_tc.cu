@@ -1017,8 +1017,11 @@ using namespace ivftq::ctc;
 
 // 0 = default (assignment on tensor cores, probes f64), 1 = f64 CUDA cores
 // only, 2 = tensor cores for probes too
-static int g_coarse_mode = 0;
-bool g_probe_tc_force = false;
+// (process-wide configuration switches, not per-call state: atomics so a
+// concurrent reader sees either value)
+#include <atomic>
+static std::atomic<int> g_coarse_mode{0};
+std::atomic<bool> g_probe_tc_force{false};
 
 extern "C" int ivftq_set_coarse_mode(int mode) {
   if (mode < 0 || mode > 2) {
@@ -1074,19 +1077,9 @@ static int coarse_gemm(const double* X, int64_t n, int dim, int L, const void* p
   const int DP = pad_dp(dim);
   const int nT = (L + tile_n(DP) - 1) / tile_n(DP);
   const size_t smem = 3 * tile_bytes(DP) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    IVFTQ_CHECK_CUDA(cudaFuncSetAttribute((const void*)coarse_tc_kernel,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * tile_bytes(128) + 1024)));
-    attr = true;
-  }
-  static int n_sms = 0;
-  if (!n_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (n_sms < 1) n_sms = 148;
-  }
+  if (int e = smem_opt_in_dev((const void*)coarse_tc_kernel, 3 * tile_bytes(128) + 1024))
+    return e;
+  const int n_sms = device_sm_count();
   const int64_t n_rt = (n + kM - 1) / kM;
   const int64_t units = n_rt * nT;
   const unsigned grid = top_v ? (unsigned)n_rt : (unsigned)(units < n_sms ? units : n_sms);
@@ -1165,12 +1158,7 @@ int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, 
   const bool fused = n_lists <= kSelRowCap;
   if (fused) {
     const size_t sm = sel_smem_bytes(n_lists, dim);
-    static size_t opted = 48 * 1024;
-    if (sm > opted) {
-      IVFTQ_CHECK_CUDA(cudaFuncSetAttribute((const void*)probe_select_kernel,
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-      opted = sm;
-    }
+    if (int e = smem_opt_in_dev((const void*)probe_select_kernel, sm)) return e;
     probe_select_kernel<<<(unsigned)nq, kSelThreads, sm, s>>>(S, qn, c64, nq, n_lists, dim, n_p,
                                                              prep, cnt, probe_out, coarse_out);
     if (int e = check_launch("probe_select")) return e;

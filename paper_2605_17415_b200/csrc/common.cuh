@@ -220,6 +220,20 @@ IVFTQ_HD bool better(double s1, int i1, double s2, int i2) {
 namespace ivftq {
 void set_error(const char* fmt, ...);
 int check_launch(const char* what);
+// Per-device state, safe for concurrent callers (mutex-guarded, keyed by the
+// calling thread's current device): the SM count, and the dynamic shared
+// memory a kernel has been opted in to on that device.
+int device_sm_count();
+int smem_opt_in_dev(const void* fn, size_t bytes);
+// A side stream and two timing-free events private to (calling thread,
+// current device): work forked off a caller's stream and joined back before
+// the call returns. Streams of other threads are never touched, so
+// concurrent calls (and one thread's graph capture) stay independent.
+struct SideStream {
+  cudaStream_t stream;
+  cudaEvent_t fork, join;
+};
+int side_stream(SideStream** out);
 }  // namespace ivftq
 
 #define IVFTQ_CHECK_CUDA(expr)                                             \

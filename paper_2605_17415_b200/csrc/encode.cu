@@ -151,10 +151,16 @@ __global__ void pack_codes_kernel(const uint8_t* __restrict__ bins,
   words[i] = word;
 }
 
-__global__ void histogram_kernel(const int32_t* __restrict__ lids, int64_t n,
+// Both kernels skip a row whose list id lies outside [0, n_lists): a corrupt
+// id from a direct C-ABI caller never writes outside the store (the Python
+// layer rejects such ids before any device work, storage.py:load_index).
+__global__ void histogram_kernel(const int32_t* __restrict__ lids, int64_t n, int n_lists,
                                  int32_t* __restrict__ counts) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) atomicAdd(&counts[lids[i]], 1);
+  if (i < n) {
+    const int l = lids[i];
+    if (l >= 0 && l < n_lists) atomicAdd(&counts[l], 1);
+  }
 }
 
 __global__ void append_kernel(ivftq_store s, const uint32_t* __restrict__ words,
@@ -165,6 +171,7 @@ __global__ void append_kernel(ivftq_store s, const uint32_t* __restrict__ words,
   if (i >= n) return;
   const int W = s.words_per_vec;
   int l = lids[i];
+  if (l < 0 || l >= s.n_lists) return;
   int r = atomicAdd(&cursor[l], 1);
   int64_t slot = s.list_offset[l] + s.list_size[l] + r;
   int64_t blk = slot >> 5;
@@ -334,7 +341,8 @@ extern "C" int ivftq_histogram(const int32_t* list_ids, int64_t n, int n_lists,
                                int32_t* counts, void* stream) {
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * n_lists, S(stream)));
   if (n == 0) return 0;
-  histogram_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(list_ids, n, counts);
+  histogram_kernel<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(list_ids, n, n_lists,
+                                                                     counts);
   return check_launch("histogram");
 }
 

@@ -1025,12 +1025,18 @@ __global__ void q16_kernel(const float* __restrict__ qrot, int64_t nq, int d, in
 }
 
 // Seed each query's global pruning bound before the scan: score the first
-// (up to) 32*P slots of the query's nearest probed list exactly as the LUT scan
-// would (f32 q_rot * f32 T, sequential, times the f32 norm, plus the f64
-// coarse score) and take the k-th best. Those are k real candidates, so the
-// query's final k-th score is at least their k-th; the margin covers the
-// difference between this f32 arithmetic and the tensor-core scan's
-// (|res| <= ~1 with ~2^-22 relative error each way). One warp per query.
+// (up to) 32*P slots of the query's nearest probed list in f32 (q_rot * f32 T,
+// four partial chains, times the f32 norm, plus the f64 coarse score) and
+// take the k-th best. Those are k real candidates, so the query's final k-th
+// score is at least their k-th -- once each seeded score is lowered by a
+// rigorous bound on how far it can sit above the tensor-core scan's score of
+// the same candidate. With S = sum_j |q_j| |T[f_j]| <= max|T| * ||q||_1, both
+// computations lie within (6d + d/4 + 19) u S of the exact dot (u = 2^-24:
+// the scan's fp32 accumulation of 3d exact fp16 products at <= 2u per add,
+// allowing for truncating tensor-core adds; its hi/lo split and dropped
+// lo*lo terms (3 * 2^-22); this kernel's four chains of d/4 terms), then one
+// rounding for the norm product. The margin uses (8d + 64) u S nrm, plus
+// 1e-12 (1 + |score|) for the f64 sum. One warp per query.
 template <int P, int FB>
 __global__ void __launch_bounds__(256)
 seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
@@ -1040,6 +1046,7 @@ seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
   constexpr int FPW = 32 / FB;
   constexpr uint32_t mask = (1u << FB) - 1u;
   __shared__ float t32[1 << FB];           // f32 level table
+  __shared__ float tmax;                   // max |T|
   __shared__ float qs_all[8][kMaxDim + 8];  // each warp's rotated query row (zero-padded)
   __shared__ double sc_all[8][32 * P];     // each warp's candidate scores
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1047,10 +1054,25 @@ seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
   for (int c = threadIdx.x; c < (1 << FB); c += blockDim.x) t32[c] = (float)levels[c];
   const int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
   float* qr = qs_all[warp];
+  float qabs = 0.f;
   if (q < nq)
-    for (int j = lane; j < W * FPW; j += 32) qr[j] = j < d ? qrot[q * d + j] : 0.f;
+    for (int j = lane; j < W * FPW; j += 32) {
+      const float v = j < d ? qrot[q * d + j] : 0.f;
+      qr[j] = v;
+      qabs += fabsf(v);
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float m = 0.f;
+    for (int c = 0; c < (1 << FB); ++c) m = fmaxf(m, fabsf(t32[c]));
+    tmax = m;
+  }
   __syncthreads();
   if (q >= nq) return;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) qabs += __shfl_xor_sync(kFull, qabs, o);
+  // S bound, rounded up generously (1.001) for the f32 sums above
+  const double slack = (double)(8 * d + 64) * 0x1p-24 * (double)tmax * (double)qabs * 1.001;
   const int l0 = probe[q * n_p];
   const int m = min(st.list_size[l0], 32 * P);
   const double cs = coarse[q * n_p];
@@ -1082,6 +1104,7 @@ seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
       const float dot = (acc[0] + acc[1]) + (acc[2] + acc[3]);
       const float nrm = __half2float(__ushort_as_half(st.norms[slot]));
       v = cs + (double)__fmul_rn(nrm, dot);
+      v -= (double)nrm * slack + 1e-12 * (1.0 + fabs(v));  // never above the scan's score
     }
     scw[p * 32 + lane] = v;
   }
@@ -1108,7 +1131,7 @@ seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
   for (int o = 16; o; o >>= 1) kth = fmax(kth, __shfl_xor_sync(kFull, kth, o));
   if (lane == 0) {
     double b = -INFINITY;
-    if (m >= k && kth > -INFINITY) b = kth - (1e-5 + 1e-5 * fabs(kth));
+    if (m >= k && kth > -INFINITY) b = kth;
     key[q] = dkey(b);
   }
 }
@@ -1124,35 +1147,89 @@ __global__ void thr_init_kernel(long long* __restrict__ key, int64_t n) {
 using namespace ivftq;
 using namespace ivftq::tc;
 
-static int g_num_sms = 0;
+// Optional device timing of the scan kernel alone (bench roofline evidence):
+// a switch and an event pair per (host thread, device), so concurrent callers
+// never record into each other's events.
+#include <map>
+#include <utility>
+static thread_local bool t_time_kernel = false;
+static thread_local std::map<int, std::pair<cudaEvent_t, cudaEvent_t>> t_ev;
 
-// Optional device timing of the scan kernel alone (bench roofline evidence).
-static bool g_time_kernel = false;
-static cudaEvent_t g_ev[2] = {nullptr, nullptr};
+static std::pair<cudaEvent_t, cudaEvent_t>* timing_events() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = t_ev.find(dev);
+  if (it == t_ev.end()) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (cudaEventCreate(&a) != cudaSuccess || cudaEventCreate(&b) != cudaSuccess) return nullptr;
+    it = t_ev.emplace(dev, std::make_pair(a, b)).first;
+  }
+  return &it->second;
+}
 
 extern "C" int ivftq_set_kernel_timing(int on) {
-  g_time_kernel = on != 0;
-  if (g_time_kernel && !g_ev[0]) {
-    IVFTQ_CHECK_CUDA(cudaEventCreate(&g_ev[0]));
-    IVFTQ_CHECK_CUDA(cudaEventCreate(&g_ev[1]));
+  t_time_kernel = on != 0;
+  if (t_time_kernel && !timing_events()) {
+    set_error("set_kernel_timing: event creation failed");
+    return IVFTQ_ERR_CUDA;
   }
   return 0;
 }
 
-extern "C" int ivftq_get_kernel_timing(void) { return g_time_kernel ? 1 : 0; }
+extern "C" int ivftq_get_kernel_timing(void) { return t_time_kernel ? 1 : 0; }
 
 extern "C" double ivftq_last_scan_kernel_ms(void) {
-  if (!g_ev[0]) return -1.0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = t_ev.find(dev);
+  if (it == t_ev.end()) return -1.0;
   float ms = -1.f;
   // events never recorded (no timed launch yet) fail here: report -1 and
   // clear the error so it does not surface at the next launch check
-  if (cudaEventSynchronize(g_ev[1]) != cudaSuccess ||
-      cudaEventElapsedTime(&ms, g_ev[0], g_ev[1]) != cudaSuccess) {
+  if (cudaEventSynchronize(it->second.second) != cudaSuccess ||
+      cudaEventElapsedTime(&ms, it->second.first, it->second.second) != cudaSuccess) {
     cudaGetLastError();
     return -1.0;
   }
   return ms;
 }
+
+// Records the start/stop events around one launch when timing is on; inside
+// a stream capture they become external event nodes, marking every replay.
+struct KernelTimer {
+  cudaStream_t s;
+  std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+  unsigned flags = cudaEventRecordDefault;
+  explicit KernelTimer(cudaStream_t st) : s(st) {
+    if (!t_time_kernel) return;
+    ev = timing_events();
+    if (!ev) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs == cudaStreamCaptureStatusActive) flags = cudaEventRecordExternal;
+    cudaEventRecordWithFlags(ev->first, s, flags);
+  }
+  void stop() {
+    if (ev) cudaEventRecordWithFlags(ev->second, s, flags);
+  }
+};
+
+// Joins the side stream back into the caller's stream on every exit path, so
+// an error return inside a capture never leaves the capture forked.
+struct SideJoin {
+  SideStream* ss;
+  cudaStream_t s;
+  bool done = false;
+  ~SideJoin() {
+    if (!done) join();
+  }
+  cudaError_t join() {
+    done = true;
+    cudaError_t e = cudaEventRecord(ss->join, ss->stream);
+    cudaError_t e2 = cudaStreamWaitEvent(s, ss->join, 0);
+    return e != cudaSuccess ? e : e2;
+  }
+};
 
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
@@ -1247,23 +1324,10 @@ extern "C" int ivftq_scan_tc_supported(int dim, int bits, int depth) {
 template <int FB, int KMAX>
 static int launch_tc(const Params& P, size_t smem, int grid, cudaStream_t s) {
   auto fn = scan_tc_kernel<FB, KMAX>;
-  cudaError_t e = cudaFuncSetAttribute((const void*)fn,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) {
-    set_error("scan_tc: smem %zu rejected: %s", smem, cudaGetErrorString(e));
-    return IVFTQ_ERR_UNSUPPORTED;
-  }
-  // inside a stream capture (IvfTqIndex's graph path) the records must be
-  // external event nodes to mark the kernel at every replay
-  unsigned rec_flags = cudaEventRecordDefault;
-  if (g_time_kernel) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cs);
-    if (cs == cudaStreamCaptureStatusActive) rec_flags = cudaEventRecordExternal;
-    cudaEventRecordWithFlags(g_ev[0], s, rec_flags);
-  }
+  if (int e = smem_opt_in_dev((const void*)fn, smem)) return e;
+  KernelTimer timer(s);
   fn<<<grid, kThreads, smem, s>>>(P);
-  if (g_time_kernel) cudaEventRecordWithFlags(g_ev[1], s, rec_flags);
+  timer.stop();
   return check_launch("scan_tc");
 }
 
@@ -1283,27 +1347,20 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
     return IVFTQ_ERR_SCRATCH;
   }
   cudaStream_t s = (cudaStream_t)stream;
-  if (!g_num_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-  }
   TcScratch S = carve_tc(scratch, nq, n_p, L, depth, st->dim);
   int64_t np = nq * n_p;
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(S.cnt2, 0, S.zero_end - (char*)S.cnt2, s));
   unsigned gp = (unsigned)((np + 255) / 256);
   // The seeded bounds and the probe regrouping both only read the probes:
-  // the seeding runs on a side stream, overlapping the (latency-bound,
-  // partly single-block) regroup kernels, and the scan waits for both.
-  static cudaStream_t side = nullptr;
-  static cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-  if (!side) {
-    IVFTQ_CHECK_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-    IVFTQ_CHECK_CUDA(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
-    IVFTQ_CHECK_CUDA(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
-  }
-  IVFTQ_CHECK_CUDA(cudaEventRecord(fork_ev, s));
-  IVFTQ_CHECK_CUDA(cudaStreamWaitEvent(side, fork_ev, 0));
+  // the seeding runs on this thread's side stream, overlapping the
+  // (latency-bound, partly single-block) regroup kernels, and the scan waits
+  // for both.
+  SideStream* ss = nullptr;
+  if (int e = side_stream(&ss)) return e;
+  cudaStream_t side = ss->stream;
+  IVFTQ_CHECK_CUDA(cudaEventRecord(ss->fork, s));
+  IVFTQ_CHECK_CUDA(cudaStreamWaitEvent(side, ss->fork, 0));
+  SideJoin join{ss, s};
   // global pruning bounds: seeded from each query's nearest list (exactness
   // preserved by a margin), unless disabled for measurement
   if (getenv("IVFTQ_NO_SEED")) {
@@ -1337,7 +1394,6 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
                                                                 S.q_lo);
     if (int e = check_launch("q16")) return e;
   }
-  IVFTQ_CHECK_CUDA(cudaEventRecord(join_ev, side));
   pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.cnt2);
   if (int e = check_launch("pair_count")) return e;
   pair_scan_kernel<<<1, 1024, 0, s>>>(S.cnt2, L, S.pstart2, S.pstart, S.ntile, S.G, S.n_items);
@@ -1351,7 +1407,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
 
   const int fb = st->field_bits, C = 1 << fb;
   const int DP = pad_dp(st->dim);
-  IVFTQ_CHECK_CUDA(cudaStreamWaitEvent(s, join_ev, 0));  // seeded bounds, A rows in place
+  IVFTQ_CHECK_CUDA(join.join());  // seeded bounds, A rows in place
   Params P{};
   const int kmax = kmax_for(depth);
   pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS, &P.nAcc);
@@ -1390,7 +1446,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   P.inv_scale = ldexpf(1.0f, -(eT + 14));
   P.lo = make_layout(P.NV, P.NS, DP, st->words_per_vec, C, kmax);
   size_t smem = P.lo.total + 1024;
-  int grid = g_num_sms;
+  int grid = device_sm_count();
   int rc;
 #define TC_CASE(FBV)                                                              \
   if (fb == FBV) {                                                                \

@@ -567,7 +567,8 @@ extern "C" int ivftq_select_topn(const double* scores, int64_t rows, int cols, i
   return check_launch("select_topn");
 }
 
-extern bool g_probe_tc_force;
+#include <atomic>
+extern std::atomic<bool> g_probe_tc_force;
 int probe_tc(const double* qn, const float* centroids, int64_t nq, int n_lists, int dim,
              int n_p, int32_t* probe_out, double* coarse_out, void* scratch,
              size_t scratch_bytes, cudaStream_t s, const void* prepared);
@@ -575,12 +576,11 @@ extern "C" size_t ivftq_probe_tc_scratch_bytes(int64_t nq, int n_lists, int dim)
 extern "C" int ivftq_coarse_tc_supported(int dim, int n_lists);
 static bool probe_tc_auto() { return ivftq_coarse_tc_supported(128, 1) != 0; }  // mode != 1
 static bool probe_tc_enabled() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool env = [] {  // thread-safe one-time read of the environment
     const char* e = getenv("IVFTQ_PROBE_TC");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1 || g_probe_tc_force;
+    return e && e[0] == '1';
+  }();
+  return env || g_probe_tc_force;
 }
 
 extern "C" size_t ivftq_probe_scratch_bytes(int64_t nq, int n_lists, int dim) {

@@ -16,6 +16,7 @@ import ctypes as C
 import gc
 import hashlib
 import os
+import threading
 import warnings
 from dataclasses import dataclass
 
@@ -566,18 +567,23 @@ class IvfTqIndex:
                 and 1 <= queries.shape[0] <= self._QUERY_CHUNK)
 
     def _search_graphed(self, queries, k, n_p, depth, rerank_depth):
-        if getattr(self, "_graph_version", None) != self._version:
-            self._graphs = {}
-            self._graph_version = self._version
+        # Graphs are per host thread: a replay overwrites its static input and
+        # output buffers, so concurrent readers of one index
+        # must never share one.
+        tls = self._thread_state()
+        if getattr(tls, "graph_version", None) != self._version:
+            tls.graphs = {}
+            tls.graph_version = self._version
+        graphs = tls.graphs
         key = (tuple(queries.shape), queries.dtype, k, n_p, depth, rerank_depth, self.scan_mode,
                self._lib.ivftq_get_kernel_timing())
-        ent = self._graphs.pop(key, None)
+        ent = graphs.pop(key, None)
         if ent is not None:
-            self._graphs[key] = ent  # most recently used last
+            graphs[key] = ent  # most recently used last
             ent[1].copy_(queries, non_blocking=True)
         else:
-            while len(self._graphs) >= self._MAX_GRAPHS:  # bound the graphs' memory pools
-                self._graphs.pop(next(iter(self._graphs)))
+            while len(graphs) >= self._MAX_GRAPHS:  # bound the graphs' memory pools
+                graphs.pop(next(iter(graphs)))
             static_in = torch.empty(queries.shape, dtype=queries.dtype, device=self.device)
             static_in.copy_(queries)
             # warm-up outside capture: library lazy state, allocator pools
@@ -590,50 +596,69 @@ class IvfTqIndex:
             gc_on = gc.isenabled()
             gc.disable()
             try:
-                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                # a per-thread capture stream: torch's default capture stream
+                # is shared by every thread
+                if getattr(tls, "capture_stream", None) is None:
+                    tls.capture_stream = torch.cuda.Stream(device=self.device)
+                with torch.cuda.graph(g, stream=tls.capture_stream,
+                                      capture_error_mode="thread_local"):
                     out = self._search_core(static_in, k, n_p, depth, rerank_depth)[:3]
             finally:
                 if gc_on:
                     gc.enable()
             ent = (g, static_in, out, self._lib.ivftq_launch_count() - c0)
-            self._graphs[key] = ent
+            graphs[key] = ent
         g, _, out, n_launch = ent
         g.replay()
         self._lib.ivftq_note_graph_launches(n_launch)
         return out
 
+    def _thread_state(self):
+        """Per-host-thread search state (side stream, graph cache)."""
+        tls = self.__dict__.get("_tls")
+        if tls is None:
+            tls = self.__dict__.setdefault("_tls", threading.local())
+        return tls
+
     def _search_core(self, queries, k, n_p, depth, rerank_depth):
         """The device sequence of one search (no host synchronisation)."""
         qn, bad, nq = self._normalize_queries_device(queries)
         dev = self.device
-        L = self.partition.n_lists
         d = self.config.dim
-        s = _lib.stream_ptr()
-        probe = torch.empty((max(nq, 1), n_p), dtype=torch.int32, device=dev)
-        coarse = torch.empty((max(nq, 1), n_p), dtype=torch.float64, device=dev)
-        pb = self._lib.ivftq_probe_scratch_bytes(nq, L, d)
-        pscr = torch.empty(pb, dtype=torch.uint8, device=dev)
         # the query rotation depends only on qn: it runs on a side stream
         # while the probe kernels run on the current one
         qrot = torch.empty((max(nq, 1), d), dtype=torch.float32, device=dev)
         cur = torch.cuda.current_stream(dev)
-        if getattr(self, "_side_stream", None) is None:
-            self._side_stream = torch.cuda.Stream(device=dev)
-        side = self._side_stream
+        tls = self._thread_state()
+        if getattr(tls, "side_stream", None) is None:
+            tls.side_stream = torch.cuda.Stream(device=dev)
+        side = tls.side_stream
         forked, rotated = torch.cuda.Event(), torch.cuda.Event()
         forked.record(cur)
         side.wait_event(forked)
         with torch.cuda.stream(side):
             self._rotate(qn, nq, qrot)
             rotated.record(side)
-        _lib.check(self._lib.ivftq_probe_prepared(
-            qn.data_ptr(), self._cent.data_ptr(), self._coarse_prep().data_ptr(), nq, L, d, n_p,
-            probe.data_ptr(), coarse.data_ptr(), pscr.data_ptr(), pb, s), "probe")
+        probe, coarse = self._probe(qn, nq, n_p)
         cur.wait_event(rotated)
         ids, scores = self._scan(qn, nq, probe, coarse, n_p, depth, qrot)
         if rerank_depth > 0:
             ids, scores = self._rerank(qn, nq, ids, depth, k)
         return ids, scores, bad, nq
+
+    def _probe(self, qn, nq, n_p):
+        """Top-n_p lists per query and their f64 coarse scores (index.py:434-438)."""
+        L = self.partition.n_lists
+        d = self.config.dim
+        probe = torch.empty((max(nq, 1), n_p), dtype=torch.int32, device=self.device)
+        coarse = torch.empty((max(nq, 1), n_p), dtype=torch.float64, device=self.device)
+        pb = self._lib.ivftq_probe_scratch_bytes(nq, L, d)
+        pscr = torch.empty(pb, dtype=torch.uint8, device=self.device)
+        _lib.check(self._lib.ivftq_probe_prepared(
+            qn.data_ptr(), self._cent.data_ptr(), self._coarse_prep().data_ptr(), nq, L, d, n_p,
+            probe.data_ptr(), coarse.data_ptr(), pscr.data_ptr(), pb, _lib.stream_ptr()),
+            "probe")
+        return probe, coarse
 
     def _coarse_prep(self):
         """Tensor-core operand images of the current centroids (made once per

@@ -11,10 +11,17 @@ shapes, sizes and value distributions BASELINE.json names:
 Queries use the same means with a separate RNG stream. Noise is drawn in
 float32 row chunks so 10M-row configs never hold a float64 copy; the chunked
 stream equals a single draw (numpy Generator fills sequentially).
+
+The 10M-row configs (`threads > 1`) draw each 1M-row chunk from its own child
+stream (`SeedSequence(seed).spawn`), so the chunks fill in parallel threads
+(numpy releases the GIL while a Generator fills an array); the rows depend only
+on the seed, never on the thread count.
 """
 
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -33,6 +40,7 @@ def mixture(
     means: np.ndarray | None = None,
     mean_seed: int | None = None,
     norm_sigma: float = 0.0,
+    threads: int = 1,
 ) -> tuple[np.ndarray, np.ndarray]:
     """Gaussian-mixture rows (float32) and the component means used.
 
@@ -42,7 +50,10 @@ def mixture(
         norm_sigma: If > 0, scale each row by a log-normal(0, norm_sigma) norm
             (config C4; the reference normalises rows, so this changes nothing
             the index sees).
+        threads: > 1 selects the chunk-parallel stream (see module docstring).
     """
+    if threads > 1:
+        return _mixture_parallel(n, d, k, sigma, seed, means, mean_seed, norm_sigma, threads)
     if means is None:
         mrng = np.random.default_rng(seed if mean_seed is None else mean_seed)
         means = mrng.standard_normal((k, d))
@@ -61,6 +72,35 @@ def mixture(
             scale = np.exp(norm_sigma * nrng.standard_normal(e - s)) / rn
             out[s:e] = (out[s:e] * scale[:, None]).astype(np.float32)
     return out, means
+
+
+def _mixture_parallel(n, d, k, sigma, seed, means, mean_seed, norm_sigma, threads):
+    if means is None:
+        mrng = np.random.default_rng(seed if mean_seed is None else mean_seed)
+        means = mrng.standard_normal((k, d))
+    out = np.empty((n, d), dtype=np.float32)
+    starts = list(range(0, n, _CHUNK))
+    kids = np.random.SeedSequence([seed, 7919]).spawn(len(starts))
+
+    def fill(i):
+        s = starts[i]
+        e = min(n, s + _CHUNK)
+        rng = np.random.default_rng(kids[i])
+        labels = rng.integers(0, len(means), e - s)
+        noise = rng.standard_normal((e - s, d), dtype=np.float32)
+        out[s:e] = (means[labels] + sigma * noise).astype(np.float32)
+        if norm_sigma > 0:
+            rn = np.linalg.norm(out[s:e].astype(np.float64), axis=1)
+            scale = np.exp(norm_sigma * rng.standard_normal(e - s)) / rn
+            out[s:e] = (out[s:e] * scale[:, None]).astype(np.float32)
+
+    with ThreadPoolExecutor(max(1, min(threads, len(starts)))) as ex:
+        list(ex.map(fill, range(len(starts))))
+    return out, means
+
+
+def gen_threads() -> int:
+    return max(1, min(16, os.cpu_count() or 1))
 
 
 @dataclass(frozen=True)
@@ -84,11 +124,13 @@ class Workload:
     query_shift: float = 0.0  # C4: per-component query mean offset scale
     norm_sigma: float = 0.0  # C4: log-normal base norms
     notes: str = ""
+    parallel: bool = False  # chunk-parallel generation (10M-row configs)
     extra: dict = field(default_factory=dict)
 
     def base(self, n: int | None = None) -> np.ndarray:
         x, _ = mixture(n or self.n, self.d, self.components, self.sigma,
-                       self.base_seed, norm_sigma=self.norm_sigma)
+                       self.base_seed, norm_sigma=self.norm_sigma,
+                       threads=gen_threads() if self.parallel else 1)
         return x
 
     def queries(self, nq: int | None = None) -> np.ndarray:
@@ -98,7 +140,8 @@ class Workload:
             srng = np.random.default_rng(self.query_seed + 1)
             means = means + self.query_shift * srng.standard_normal(means.shape)
         q, _ = mixture(nq or self.n_queries, self.d, self.components, self.sigma,
-                       self.query_seed, means=means)
+                       self.query_seed, means=means,
+                       threads=gen_threads() if self.parallel else 1)
         return q
 
 
@@ -108,14 +151,23 @@ WORKLOADS = {
     "c2": Workload("c2", 1_000_000, 128, 1000, 0.3, 1024, 4, 10_000, 10,
                    (1, 4, 16, 64), kmeans_sample=100_000,
                    notes="configs[1]: k-means on a seeded 100k subsample"),
+    # C3: the north_star target. k-means (reference algorithm, host f64) runs on
+    # a seeded 32,768-row subsample (8 rows per list) so the bench's two arms
+    # train the identical centroids on the host in ~half a minute.
     "c3": Workload("c3", 10_000_000, 96, 4096, 0.3, 4096, 4, 10_000, 10,
-                   (16, 32, 64, 128), kmeans_sample=1_000_000,
+                   (16, 32, 64, 128), kmeans_sample=32_768, parallel=True,
                    notes="configs[2]: sigma unspecified, 0.3 recorded"),
+    # C3 with overlapping clusters: 1024 mixture components spread over 4096
+    # lists and sigma 0.6, so true neighbours straddle lists and recall rises
+    # with n_p (the C3 mixture puts every neighbour in the nearest list).
+    "c3_hard": Workload("c3_hard", 10_000_000, 96, 1024, 0.6, 4096, 4, 10_000, 10,
+                        (16, 32, 64, 128), kmeans_sample=32_768, parallel=True,
+                        notes="harder C3 variant: K=1024 components, sigma 0.6"),
     "c4": Workload("c4", 10_000_000, 200, 4096, 0.3, 4096, 4, 10_000, 10, (64,),
-                   kmeans_sample=1_000_000, query_shift=0.5, norm_sigma=0.25,
+                   kmeans_sample=32_768, query_shift=0.5, norm_sigma=0.25, parallel=True,
                    notes="configs[3]: queries from means + 0.5*N(0,1) offsets"),
     "c5": Workload("c5", 10_000_000, 96, 4096, 0.3, 4096, 4, 10_000, 10, (32,),
-                   kmeans_sample=1_000_000,
+                   kmeans_sample=1_000_000, parallel=True,
                    notes="configs[4]: stream of 1M batches, L=4096 recorded"),
 }
 

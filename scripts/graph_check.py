@@ -20,4 +20,4 @@ for n_p in (8, 64):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize(); t = time.perf_counter()
             e0.record(); idx.search_batch(Qd, 10, n_p, return_device=True); e1.record(); torch.cuda.synchronize()
-            print(n_p, graphs, r, round(e0.elapsed_time(e1), 3), "ms gpu", round((time.perf_counter()-t)*1e3, 3), "ms host", len(getattr(idx, '_graphs', {}) or {}), flush=True)
+            print(n_p, graphs, r, round(e0.elapsed_time(e1), 3), "ms gpu", round((time.perf_counter()-t)*1e3, 3), "ms host", len(getattr(idx._thread_state(), 'graphs', {}) or {}), flush=True)

@@ -621,7 +621,7 @@ def test_graph_replay_equals_eager(golden):
         (ei, es), (ri, rs) = both(q)
         np.testing.assert_array_equal(ei, ri)
         np.testing.assert_array_equal(es, rs)
-    assert len(idx._graphs) == 1
+    assert len(idx._thread_state().graphs) == 1
     dev_ids, _ = idx.search_batch(torch.from_numpy(q).cuda(), 10, 8, return_device=True)
     idx.search_batch(torch.from_numpy(q[::-1].copy()).cuda(), 10, 8)  # next replay
     np.testing.assert_array_equal(dev_ids.cpu().numpy(), ei)  # returned tensors are owned

@@ -134,3 +134,24 @@ def test_product_never_imports_oracle():
     for p in pkg.rglob("*.py"):
         assert not re.search(r"^\s*(from|import)\s+\.*oracle", p.read_text(), re.M), p
         assert "ivftq_oracle" not in p.read_text(), p
+
+
+def test_load_rejects_out_of_range_list_id(golden, tmp_path):
+    """A corrupt list id fails cleanly before any device work (ADVICE r1:
+    the id would index device list buffers)."""
+    import struct
+
+    from paper_2605_17415_b200.storage import _CFG, IndexFormatError, load_index
+
+    raw = bytearray(golden("d32_b4_L16_raw")["ivtq_bytes"].tobytes())
+    dim, bits, n_lists, flags, _, _, count = struct.unpack_from(_CFG, raw, 6)
+    lv = 1 << bits
+    off = 6 + struct.calcsize(_CFG) + 8 * (lv + 1 + lv + 2 * lv) + 16 + 8 * dim * dim \
+        + 4 * n_lists * dim
+    for bad in (n_lists, 0x80000000):
+        b = bytearray(raw)
+        struct.pack_into("<I", b, off + 4 * 3, bad)  # list id of vector 3
+        p = tmp_path / "x.ivtq"
+        p.write_bytes(bytes(b))
+        with pytest.raises(IndexFormatError, match="list id .* of vector 3 out of range"):
+            load_index(p)
