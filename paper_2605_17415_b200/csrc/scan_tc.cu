@@ -636,6 +636,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
         const int ks = DP / 16;
         const uint64_t dstep = (2 * b_lbo) >> 4;
         const uint64_t dh = sm100::smem_desc(bh, b_lbo, sbo), dl = sm100::smem_desc(bl, b_lbo, sbo);
+#ifdef IVFTQ_EXP_NOMMA
+        if (c.nqt < 0)  // experiment build: MMAs skipped (timing bound only)
+#endif
 #pragma unroll 1
         for (int pass = 0; pass < 3; ++pass) {
           const uint32_t at = pass == 1 ? qlo_t : qhi_t;
@@ -706,6 +709,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       unsigned char* bhi = smem + (ob ? Lo.bhi[1] : Lo.bhi[0]);
       unsigned char* blo = smem + (ob ? Lo.blo[1] : Lo.blo[0]);
       const int nvshift = __ffs(NV) - 1;
+#ifdef IVFTQ_EXP_NODEC
+      if (c.nqt < 0)  // experiment build: decode skipped (timing bound only)
+#endif
       for (int task = dt_; task < NV * NG; task += kDecThreads) {
         const int v = task & (NV - 1), gi = task >> nvshift;
         const uint32_t* wv = cw + (v >> 5) * W * 32 + (v & 31);
@@ -793,7 +799,11 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       const int c0 = half * cols;
       // a warp whose 32 query rows all lie past the item's queries (zero A
       // rows) has nothing to take: it skips the tile and frees its issue slots
+#ifdef IVFTQ_EXP_NOEPI
+      const int cols_here = 0;  // experiment build: epilogue skipped (timing bound only)
+#else
       const int cols_here = quad * 32 < c.nqt ? cols : 0;
+#endif
 #pragma unroll 1
       for (int cc = 0; cc < cols_here; cc += IVFTQ_EPI_LD) {
         uint32_t r[IVFTQ_EPI_LD];

@@ -1,5 +1,6 @@
 """Run one C2-like batched search with the scan_tc timeline trace enabled."""
 import os, sys, time
+os.environ["IVFTQ_NO_GRAPH"] = "1"  # a graph replay would skip the host-side trace dump
 from pathlib import Path
 # the timeline instrumentation only exists in the trace build (make -C paper_2605_17415_b200/csrc trace)
 os.environ.setdefault("IVFTQ_LIB", str(Path(__file__).resolve().parents[1] / "paper_2605_17415_b200" / "lib" / "libivftq_b200_trace.so"))
