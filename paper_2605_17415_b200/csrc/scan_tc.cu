@@ -51,6 +51,13 @@ void launch_merge(const double* part_s, const int32_t* part_id, int64_t nq, int 
                   int64_t* ids_out, double* s_out, cudaStream_t s,
                   const int32_t* counts = nullptr);
 int merge_smem_opt_in(int K);
+// scan_vq.cu: the vectors x queries scan (d <= 128)
+bool scan_vq_supported(int dim, int field_bits_, int depth);
+int launch_scan_vq(const ivftq_store* st, const double* coarse, const double* levels,
+                   const int32_t* pairs, const int32_t* pstart, const int2* items,
+                   const int32_t* n_items, int32_t* counter, double* part_s, int32_t* part_id,
+                   int32_t* qcnt, long long* thr_key, const uint32_t* q_hi, const uint32_t* q_lo,
+                   int n_p, int depth, int qcap, cudaStream_t s);
 
 namespace tc {
 
@@ -1418,6 +1425,22 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   const int fb = st->field_bits, C = 1 << fb;
   const int DP = pad_dp(st->dim);
   IVFTQ_CHECK_CUDA(join.join());  // seeded bounds, A rows in place
+  if (scan_vq_supported(st->dim, fb, depth)) {
+    const int qcap = n_p * depth;  // one partial list per (query, list) pair
+    int rc;
+    {
+      KernelTimer timer(s);
+      rc = launch_scan_vq(st, coarse, levels, S.pairs, S.pstart, S.items, S.n_items, S.counter,
+                          S.part_s, S.part_id, S.qcnt, S.thr_key, S.q_hi, S.q_lo, n_p, depth,
+                          qcap, s);
+      timer.stop();
+    }
+    if (rc) return rc;
+    if (int e = merge_smem_opt_in(depth)) return e;
+    // fixed k-slot per pair, empty entries id INT_MAX: no per-query counts
+    launch_merge(S.part_s, S.part_id, nq, qcap, depth, ids_out, scores_out, s, nullptr);
+    return check_launch("merge");
+  }
   Params P{};
   const int kmax = kmax_for(depth);
   pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS, &P.nAcc);
