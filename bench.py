@@ -434,6 +434,9 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
+    prof_steps = os.environ.get("IVFTQ_PROFILE_STEPS") == "1"  # ncu --profile-from-start off
+    if prof_steps:
+        torch.cuda.profiler.start()
     for _ in range(args.steps):
         flush.fill_(1)
         torch.cuda.synchronize()
@@ -444,6 +447,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         launches += L.ivftq_launch_count() - c0
         times.append(e0.elapsed_time(e1))
+    if prof_steps:
+        torch.cuda.profiler.stop()
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
@@ -531,7 +536,8 @@ def run_ours(args):
             # per-query code stream a query-major scan would read.
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / tf, "traffic": traffic,
-                         "kernel": "scan_tc_kernel", "peak_source": src + " bf16 dense",
+                         "kernel": L.ivftq_last_scan_kernel().decode(),
+                         "peak_source": src + " bf16 dense",
                          "alg_flops_per_launch": alg_flops, "kernel_ms": t_kernel * 1000,
                          "pairs_per_launch": vq, "alg_bytes_per_launch": alg_bytes,
                          "bytes_per_vector": s_vec, "store_bytes": store_bytes,

@@ -219,6 +219,9 @@ int ivftq_set_kernel_timing(int on);
  * it was captured with timing on; the host keys its graphs on this). */
 int ivftq_get_kernel_timing(void);
 double ivftq_last_scan_kernel_ms(void);
+/* Name of the list-scan kernel the calling thread's last tensor-core scan ran
+ * ("scan_vq_kernel" or "scan_tc_kernel"); "" before the first. */
+const char* ivftq_last_scan_kernel(void);
 /* Exact re-score of the top-depth candidates against the raw f32 store and
  * re-order to top-k (index.py:470-473). */
 int ivftq_rerank(const float* raw, const double* qn, const int64_t* cand_ids,

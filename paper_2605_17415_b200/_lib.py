@@ -90,6 +90,7 @@ _SIGS = {
     "ivftq_get_kernel_timing": (_i32, []),
     "ivftq_set_kernel_timing": (_i32, [_i32]),
     "ivftq_last_scan_kernel_ms": (C.c_double, []),
+    "ivftq_last_scan_kernel": (C.c_char_p, []),
     "ivftq_scan_tc_scratch_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "ivftq_rerank": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
     "ivftq_decode_scratch_bytes": (_sz, [_i64, _i32]),

@@ -1170,6 +1170,9 @@ using namespace ivftq::tc;
 #include <map>
 #include <utility>
 static thread_local bool t_time_kernel = false;
+static thread_local const char* t_scan_kernel = "";
+
+extern "C" const char* ivftq_last_scan_kernel(void) { return t_scan_kernel; }
 static thread_local std::map<int, std::pair<cudaEvent_t, cudaEvent_t>> t_ev;
 
 static std::pair<cudaEvent_t, cudaEvent_t>* timing_events() {
@@ -1425,7 +1428,14 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   const int fb = st->field_bits, C = 1 << fb;
   const int DP = pad_dp(st->dim);
   IVFTQ_CHECK_CUDA(join.join());  // seeded bounds, A rows in place
-  if (scan_vq_supported(st->dim, fb, depth)) {
+  // The vectors x queries scan sizes the MMA N to the queries a list really
+  // has; with 128+ queries per list on average (C2: ~625) every item of the
+  // queries-on-M scan is full and its fused per-query top-k wins, so the
+  // choice follows the batch shape (both return the exact same top-k).
+  const char* force_vq = getenv("IVFTQ_SCAN_VQ");
+  const bool vq_shape = force_vq ? atoi(force_vq) != 0 : (double)nq * n_p < 128.0 * L;
+  if (vq_shape && scan_vq_supported(st->dim, fb, depth)) {
+    t_scan_kernel = "scan_vq_kernel";
     const int qcap = n_p * depth;  // one partial list per (query, list) pair
     int rc;
     {
@@ -1441,6 +1451,7 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
     launch_merge(S.part_s, S.part_id, nq, qcap, depth, ids_out, scores_out, s, nullptr);
     return check_launch("merge");
   }
+  t_scan_kernel = "scan_tc_kernel";
   Params P{};
   const int kmax = kmax_for(depth);
   pick_tile(DP, st->words_per_vec, C, kmax, &P.NV, &P.NS, &P.nAcc);

@@ -84,17 +84,27 @@ def _tc_ok(idx, depth):
     return bool(_lib.lib().ivftq_scan_tc_supported(idx.config.dim, idx.config.bits, depth))
 
 
-@pytest.mark.parametrize("mode", ["lut", "tc"])
+def _set_mode(idx, mode, monkeypatch):
+    """lut, or the tensor-core scan with its kernel forced: tc_vq (vectors x
+    queries, scan_vq.cu) or tc_qm (queries x vectors, scan_tc.cu)."""
+    if mode.startswith("tc"):
+        monkeypatch.setenv("IVFTQ_SCAN_VQ", "1" if mode == "tc_vq" else "0")
+        idx.scan_mode = "tc"
+    else:
+        idx.scan_mode = mode
+
+
+@pytest.mark.parametrize("mode", ["lut", "tc_vq", "tc_qm"])
 @pytest.mark.parametrize("name", SMALL)
-def test_search_matches_reference(golden, name, mode):
+def test_search_matches_reference(golden, name, mode, monkeypatch):
     g = golden(name)
     idx = index_from_golden(g)
-    idx.scan_mode = mode
+    _set_mode(idx, mode, monkeypatch)
     idx.add_batch(g["x"])
     ran = 0
     for (k, n_p, rr) in _search_keys(g):
         depth = max(k, rr) if rr else k
-        if mode == "tc" and not _tc_ok(idx, depth):
+        if mode != "lut" and not _tc_ok(idx, depth):
             continue
         ran += 1
         with warnings.catch_warnings():
@@ -102,7 +112,7 @@ def test_search_matches_reference(golden, name, mode):
             ids, sc = idx.search_batch(g["queries"], k, n_p, rr)
         assert ids.dtype == np.int64 and sc.dtype == np.float64
         compare_topk(ids, sc, g[f"s_{k}_{n_p}_{rr}_ids"], g[f"s_{k}_{n_p}_{rr}_scores"])
-    if mode == "tc" and not ran:
+    if mode != "lut" and not ran:
         pytest.skip("no tensor-core-eligible case (bits or depth)")
 
 
@@ -127,12 +137,12 @@ def test_probes_identical(golden):
     np.testing.assert_allclose(coarse.cpu().numpy(), ref, rtol=0, atol=1e-15)
 
 
-@pytest.mark.parametrize("mode", ["lut", "tc"])
+@pytest.mark.parametrize("mode", ["lut", "tc_vq", "tc_qm"])
 @pytest.mark.parametrize("seed,d,bits,L,sign", [(1, 48, 4, 24, True), (2, 100, 3, 40, True),
                                                   (3, 64, 2, 16, False), (4, 130, 4, 8, True),
                                                   (5, 33, 6, 12, True), (6, 20, 7, 6, False),
                                                   (7, 200, 4, 32, True), (8, 96, 4, 64, True)])
-def test_random_configs_against_oracle(seed, d, bits, L, sign, mode):
+def test_random_configs_against_oracle(seed, d, bits, L, sign, mode, monkeypatch):
     """Fresh seeded inputs, oracle restatement as the checker."""
     from oracle import ivftq_oracle as orc
     from paper_2605_17415_b200 import (CoarsePartition, IndexConfig, IvfTqIndex,
@@ -147,9 +157,9 @@ def test_random_configs_against_oracle(seed, d, bits, L, sign, mode):
     R = generate_rotation(d, seed)
     cfg = IndexConfig(dim=d, bits=bits, n_lists=L, use_sign_bit=sign, keep_raw=True)
     idx = IvfTqIndex(cfg, q, R, CoarsePartition(L, d, cent))
-    if mode == "tc" and not _tc_ok(idx, 15):
+    if mode != "lut" and not _tc_ok(idx, 15):
         pytest.skip("bits outside the tensor-core path")
-    idx.scan_mode = mode
+    _set_mode(idx, mode, monkeypatch)
     idx.add_batch(x[:1000])
     idx.add_batch(x[1000:])
     o = orc.OracleIndex(cent, R.matrix, q.boundaries, q.centroids, q.half_bin_means,
