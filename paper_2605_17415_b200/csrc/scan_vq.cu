@@ -264,6 +264,15 @@ __device__ __forceinline__ uint32_t ld_vol(const uint32_t* p) {
   return *(volatile const uint32_t*)p;
 }
 
+// Roles that usually run ahead (producer, loader, decoders, emitter) poll
+// with a short sleep, so their waits do not take issue slots from the
+// epilogue warps sharing their SM sub-partition.
+#ifndef IVFTQ_VQ_SLEEP
+#define IVFTQ_VQ_SLEEP 64
+#endif
+__device__ __forceinline__ void vwait_sleep(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) __nanosleep(IVFTQ_VQ_SLEEP);
+}
 // mbarrier wait; the debug build (make debug) reports a wait that never ends
 #ifdef IVFTQ_DEBUG
 __shared__ int dbg_state[32];  // per warp: tag * 1000000 + tile counter
@@ -282,10 +291,12 @@ __device__ __forceinline__ void vwait(uint64_t* bar, uint32_t parity, int tag) {
   if ((threadIdx.x & 31) == 0) dbg_state[threadIdx.x >> 5] = -tag;
 }
 #define VWAIT(bar, parity, tag) vwait(bar, parity, tag)
+#define VWAITS(bar, parity, tag) vwait(bar, parity, tag)
 #define DSTATE(v) do { if ((threadIdx.x & 31) == 0) dbg_state[threadIdx.x >> 5] = (v); } while (0)
 #else
 #define DSTATE(v) do {} while (0)
 #define VWAIT(bar, parity, tag) sm100::mbar_wait(bar, parity)
+#define VWAITS(bar, parity, tag) vwait_sleep(bar, parity)
 #endif
 
 // Decode one K half (dims [KH*DP/2, (KH+1)*DP/2)) of one vector into TMEM:
@@ -413,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
         int item = 0;
         if (lane == 0) item = atomicAdd(P.counter, 1);
         item = __shfl_sync(kFull, item, 0);
-        if (jf >= (uint32_t)kItems) VWAIT(&it_empty[jf % kItems], ((jf / kItems) - 1) & 1, 1);
+        if (jf >= (uint32_t)kItems) VWAITS(&it_empty[jf % kItems], ((jf / kItems) - 1) & 1, 1);
         ItemRec* rec = rec_at(jf);
         if (item >= n_items) {
           if (lane == 0) {
@@ -480,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
       __syncwarp();
       if (l < 0) {
         const int s = t % NS;
-        if (t >= (uint32_t)NS) VWAIT(&st_empty[s], ((t / NS) - 1) & 1, 2);
+        if (t >= (uint32_t)NS) VWAITS(&st_empty[s], ((t / NS) - 1) & 1, 2);
         if (lane == 0) {
           ((Ctrl*)(stage(s) + Lo.st_ctrl))->list = -1;
           sm100::mbar_arrive(&st_full[s]);
@@ -489,7 +500,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
       }
       for (int i = 0; i < ntiles; ++i, ++t) {
         const int s = t % NS;
-        if (t >= (uint32_t)NS) VWAIT(&st_empty[s], ((t / NS) - 1) & 1, 3);
+        if (t >= (uint32_t)NS) VWAITS(&st_empty[s], ((t / NS) - 1) & 1, 3);
         if (lane == 0) {
           unsigned char* sp = stage(s);
           Ctrl* c = (Ctrl*)(sp + Lo.st_ctrl);
@@ -519,12 +530,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
     // image first, lo image DP*kQM*2 bytes later. Rows past nq are zero.
     constexpr int NCH = DP / 8;
     for (uint32_t j = 0;; ++j) {
-      VWAIT(&it_full[j % kItems], (j / kItems) & 1, 4);
+      VWAITS(&it_full[j % kItems], (j / kItems) & 1, 4);
       const ItemRec* rec = rec_at(j);
       const int l = rec->list, nq = rec->nq, N = rec->N;
       if (l < 0) break;
       const int b = j & 1;
-      if (j >= 2) VWAIT(&b_empty[b], ((j >> 1) - 1) & 1, 5);
+      if (j >= 2) VWAITS(&b_empty[b], ((j >> 1) - 1) & 1, 5);
       unsigned char* bq = smem + (b ? Lo.bq[1] : Lo.bq[0]);
       const int total = N * NCH * 2;
 #pragma unroll 1
@@ -604,14 +615,14 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
     uint32_t t = 0;
     for (;;) {
       const int s = t % NS, ab = t & 1;
-      VWAIT(&st_full[s], (t / NS) & 1, 9);
+      VWAITS(&st_full[s], (t / NS) & 1, 9);
       if (warp == kDec0) VTRACE(6, clock64());
       unsigned char* sp = stage(s);
       const Ctrl c = *(const Ctrl*)(sp + Lo.st_ctrl);
       if (kh == 0) {
         // tile record for the MMA issuer and the epilogue: the stage slot
         // goes back to the producer as soon as this tile is decoded
-        if (t >= (uint32_t)kMeta) VWAIT(&meta_empty[t % kMeta], ((t / kMeta) - 1) & 1, 10);
+        if (t >= (uint32_t)kMeta) VWAITS(&meta_empty[t % kMeta], ((t / kMeta) - 1) & 1, 10);
         unsigned char* mp = meta_at(t);
         if (warp == kDec0 && lane == 0) *(Ctrl*)mp = c;
         if (c.list >= 0) {
@@ -624,7 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&meta_full[t % kMeta]);
       }
-      if (t >= 2) VWAIT(&a_empty[ab], ((t >> 1) - 1) & 1, 11);  // (also before a stop: parity)
+      if (t >= 2) VWAITS(&a_empty[ab], ((t >> 1) - 1) & 1, 11);  // (also before a stop: parity)
       if (c.list < 0) {
         __syncwarp();
         if (lane == 0) sm100::mbar_arrive(&a_full[ab]);
@@ -849,7 +860,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
       }
     };
     for (uint32_t j = 0;; ++j) {
-      VWAIT(&it_full[j % kItems], (j / kItems) & 1, 15);
+      VWAITS(&it_full[j % kItems], (j / kItems) & 1, 15);
       const bool stop = rec_at(j)->list < 0;
       if (j >= 2) {  // slot j & 1 is free once item j-2 is done
         const uint32_t e = j - 2;
