@@ -109,6 +109,42 @@ size_t ivftq_assign_tc_scratch_bytes(int64_t n, int n_lists, int dim);
 int ivftq_assign_tc(const double* xn, const float* centroids, int64_t n, int n_lists,
                     int dim, int32_t* list_out, void* scratch, size_t scratch_bytes,
                     void* stream);
+/* ---- GPU spherical k-means for the partition refresh (partition.py:64-178,
+ * refresh.py:171-175): seeding, Lloyd assignment, Lloyd sums -------------- */
+/* Lloyd-step assignment on f64 centroids (partition.py:149-150): the same
+ * tensor-core pass + exact f64 decision as ivftq_assign_tc, ties to the lower
+ * list. scratch >= ivftq_assign_tc_scratch_bytes(n, n_lists, dim). */
+int ivftq_assign_tc64(const double* xn, const double* centroids, int64_t n, int n_lists,
+                      int dim, int32_t* list_out, void* scratch, size_t scratch_bytes,
+                      void* stream);
+/* k-means++ seeding (partition.py:_kmeanspp, 83-113) entirely on the device.
+ * X (n, dim) f64 unit rows; `first` = the host's rng.integers(n);
+ * host_uniforms (k-1, nc) = the host's rng.random(nc) of every step in order,
+ * nc = ivftq_kmeanspp_candidates(k) = 2 + floor(log2 k). chosen_out[k]
+ * (device) receives the centre rows; totals_out[k] (device) the potential
+ * total before each step (entry 0 unused): a total <= 1e-12 means the
+ * reference's degenerate branch applies and the caller must seed on its
+ * checked path instead. */
+int ivftq_kmeanspp_candidates(int k);
+size_t ivftq_kmeanspp_scratch_bytes(int64_t n, int dim, int k);
+int ivftq_kmeanspp_seed(const double* X, int64_t n, int dim, int k, int64_t first,
+                        const double* host_uniforms, int64_t* chosen_out,
+                        double* totals_out, void* scratch, size_t scratch_bytes,
+                        void* stream);
+/* Lloyd update (partition.py:153-160): counts_out[l] rows per list and
+ * sums_out[l] = the list's rows, in ascending row order, added in the order
+ * of np.add.reduceat over the stably sorted rows (first row + numpy's pairwise
+ * sum of the rest): bit-identical f64 sums. */
+size_t ivftq_kmeans_sums_scratch_bytes(int64_t n, int n_lists);
+int ivftq_kmeans_sums(const double* X, const int32_t* list_ids, int64_t n, int dim,
+                      int n_lists, double* sums_out, int32_t* counts_out, void* scratch,
+                      size_t scratch_bytes, void* stream);
+/* out[i] = x_i . C[list_ids[i]] (partition.py:162, the empty-list rule's key). */
+int ivftq_rowdot64(const double* X, const double* C, const int32_t* list_ids, int64_t n,
+                   int dim, double* out, void* stream);
+/* *differ (device) = 1 when the two assignments differ anywhere (partition.py:151). */
+int ivftq_lists_differ(const int32_t* a, const int32_t* b, int64_t n, int32_t* differ,
+                       void* stream);
 /* Coarse-scoring path selection (results are identical in every mode):
  * 0 = default: assignment and probes on tensor cores with the exact f64 guard
  *     band whenever the shape is supported (padded dim <= 256, n_p <= 128),

@@ -72,6 +72,14 @@ _SIGS = {
     "ivftq_probe_scratch_bytes": (_sz, [_i64, _i32, _i32]),
     "ivftq_assign_tc_scratch_bytes": (_sz, [_i64, _i32, _i32]),
     "ivftq_assign_tc": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _sz, _vp]),
+    "ivftq_assign_tc64": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _sz, _vp]),
+    "ivftq_kmeanspp_candidates": (_i32, [_i32]),
+    "ivftq_kmeanspp_scratch_bytes": (_sz, [_i64, _i32, _i32]),
+    "ivftq_kmeanspp_seed": (_i32, [_vp, _i64, _i32, _i32, _i64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ivftq_kmeans_sums_scratch_bytes": (_sz, [_i64, _i32]),
+    "ivftq_kmeans_sums": (_i32, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _sz, _vp]),
+    "ivftq_rowdot64": (_i32, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "ivftq_lists_differ": (_i32, [_vp, _vp, _i64, _vp, _vp]),
     "ivftq_set_coarse_mode": (_i32, [_i32]),
     "ivftq_coarse_tc_supported": (_i32, [_i32, _i32]),
     "ivftq_coarse_prep_bytes": (_sz, [_i32, _i32]),

@@ -63,7 +63,8 @@ __device__ __forceinline__ void split16(float x, uint16_t& hi, uint16_t& lo) {
   lo = __half_as_ushort(__float2half_rn(x - __half2float(h)));
 }
 
-__global__ void prep_stats_kernel(const float* __restrict__ c, int L, int d,
+template <typename CT>
+__global__ void prep_stats_kernel(const CT* __restrict__ c, int L, int d,
                                   PrepHeader* __restrict__ hdr) {
   // one warp per centroid (coalesced row reads)
   const int lane = threadIdx.x & 31;
@@ -71,7 +72,7 @@ __global__ void prep_stats_kernel(const float* __restrict__ c, int L, int d,
   if (l >= L) return;
   float mx = 0.f, ss = 0.f;
   for (int j = lane; j < d; j += 32) {
-    const float v = c[(int64_t)l * d + j];
+    const float v = (float)c[(int64_t)l * d + j];
     mx = fmaxf(mx, fabsf(v));
     ss = fmaf(v, v, ss);
   }
@@ -87,7 +88,8 @@ __global__ void prep_stats_kernel(const float* __restrict__ c, int L, int d,
 }
 
 // one thread per (centroid, 8-wide k chunk)
-__global__ void prep_split_kernel(const float* __restrict__ c, int L, int d, int DP, int nT,
+template <typename CT>
+__global__ void prep_split_kernel(const CT* __restrict__ c, int L, int d, int DP, int nT,
                                   PrepHeader* __restrict__ hdr, unsigned char* __restrict__ img) {
   const int NB = tile_n(DP), NCH = DP / 8;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -106,7 +108,7 @@ __global__ void prep_split_kernel(const float* __restrict__ c, int L, int d, int
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int k = ch * 8 + e;
-    const float x = (l < L && k < d) ? c[(int64_t)l * d + k] * sc : 0.f;
+    const float x = (l < L && k < d) ? (float)c[(int64_t)l * d + k] * sc : 0.f;
     split16(x, hi[e], lo[e]);
   }
   unsigned char* t = img + (size_t)tile * tile_bytes(DP);
@@ -117,7 +119,8 @@ __global__ void prep_split_kernel(const float* __restrict__ c, int L, int d, int
                                                       lo[4] | (lo[5] << 16), lo[6] | (lo[7] << 16));
 }
 
-__global__ void prep_c64_kernel(const float* __restrict__ c, int64_t n, double* __restrict__ out) {
+template <typename CT>
+__global__ void prep_c64_kernel(const CT* __restrict__ c, int64_t n, double* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = (double)c[i];
 }
@@ -1041,23 +1044,31 @@ extern "C" size_t ivftq_coarse_prep_bytes(int n_lists, int dim) {
   return c64_offset(n_lists, dim) + (size_t)n_lists * dim * sizeof(double);
 }
 
-extern "C" int ivftq_coarse_prepare(const float* centroids, int n_lists, int dim, void* prep,
-                                    void* stream) {
+// CT = float: the index's centroids; CT = double: the f64 centroids of a Lloyd
+// iteration (the images are built from their f32 roundings, 2^-24 relative,
+// far inside the guard band; the exact re-scoring reads the f64 values).
+template <typename CT>
+static int coarse_prepare_t(const CT* centroids, int n_lists, int dim, void* prep, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   const int DP = pad_dp(dim);
   const int nT = (n_lists + tile_n(DP) - 1) / tile_n(DP);
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(prep, 0, kHeader, s));
-  prep_stats_kernel<<<(n_lists + 7) / 8, 256, 0, s>>>(centroids, n_lists, dim,
-                                                         (PrepHeader*)prep);
+  prep_stats_kernel<CT><<<(n_lists + 7) / 8, 256, 0, s>>>(centroids, n_lists, dim,
+                                                             (PrepHeader*)prep);
   if (int e = check_launch("coarse_prep_stats")) return e;
   const int64_t work = (int64_t)nT * tile_n(DP) * (DP / 8);
-  prep_split_kernel<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(
+  prep_split_kernel<CT><<<(unsigned)((work + 255) / 256), 256, 0, s>>>(
       centroids, n_lists, dim, DP, nT, (PrepHeader*)prep, (unsigned char*)prep + kHeader);
   if (int e = check_launch("coarse_prep_split")) return e;
   const int64_t nc = (int64_t)n_lists * dim;
-  prep_c64_kernel<<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(
+  prep_c64_kernel<CT><<<(unsigned)((nc + 255) / 256), 256, 0, s>>>(
       centroids, nc, (double*)((unsigned char*)prep + c64_offset(n_lists, dim)));
   return check_launch("coarse_prep_c64");
+}
+
+extern "C" int ivftq_coarse_prepare(const float* centroids, int n_lists, int dim, void* prep,
+                                    void* stream) {
+  return coarse_prepare_t<float>(centroids, n_lists, dim, prep, stream);
 }
 
 // S' (optional) and per-row best four (optional) for rows X[0..n)
@@ -1095,12 +1106,9 @@ extern "C" size_t ivftq_assign_tc_scratch_bytes(int64_t n, int n_lists, int dim)
          1024 + (size_t)n * pad_dp(dim) * 4 + 256;
 }
 
-extern "C" int ivftq_assign_tc(const double* xn, const float* centroids, int64_t n, int n_lists,
-                               int dim, int32_t* list_out, void* scratch, size_t scratch_bytes,
-                               void* stream) {
-  if (n == 0) return 0;
-  if (!ivftq_coarse_tc_supported(dim, n_lists))
-    return ivftq_assign(xn, centroids, n, n_lists, dim, list_out, stream);
+template <typename CT>
+static int assign_tc_t(const double* xn, const CT* centroids, int64_t n, int n_lists, int dim,
+                       int32_t* list_out, void* scratch, size_t scratch_bytes, void* stream) {
   if (scratch_bytes < ivftq_assign_tc_scratch_bytes(n, n_lists, dim)) {
     set_error("assign_tc: scratch too small");
     return IVFTQ_ERR_SCRATCH;
@@ -1115,7 +1123,7 @@ extern "C" int ivftq_assign_tc(const double* xn, const float* centroids, int64_t
   int32_t* nfull = full + n;
   uint32_t* xsplit = (uint32_t*)(((uintptr_t)(nfull + 1) + 255) & ~(uintptr_t)255);
   IVFTQ_CHECK_CUDA(cudaMemsetAsync(nfull, 0, sizeof(int32_t), s));
-  if (int e = ivftq_coarse_prepare(centroids, n_lists, dim, prep, stream)) return e;
+  if (int e = coarse_prepare_t<CT>(centroids, n_lists, dim, prep, stream)) return e;
   if (int e = coarse_gemm(xn, n, dim, n_lists, prep, nullptr, tv, ti, s, xsplit)) return e;
   const double* c64 = (const double*)(prep + c64_offset(n_lists, dim));
   assign_exact_kernel<<<(unsigned)((n * kTopA + 127) / 128), 128, 0, s>>>(xn, c64, n, dim,
@@ -1126,6 +1134,30 @@ extern "C" int ivftq_assign_tc(const double* xn, const float* centroids, int64_t
   if (int e = check_launch("assign_pick")) return e;
   assign_full_kernel<<<148, 256, 0, s>>>(xn, c64, n_lists, dim, full, nfull, list_out);
   return check_launch("assign_full");
+}
+
+extern "C" int ivftq_assign_tc(const double* xn, const float* centroids, int64_t n, int n_lists,
+                               int dim, int32_t* list_out, void* scratch, size_t scratch_bytes,
+                               void* stream) {
+  if (n == 0) return 0;
+  if (!ivftq_coarse_tc_supported(dim, n_lists))
+    return ivftq_assign(xn, centroids, n, n_lists, dim, list_out, stream);
+  return assign_tc_t<float>(xn, centroids, n, n_lists, dim, list_out, scratch, scratch_bytes,
+                            stream);
+}
+
+// The Lloyd-step assignment of the GPU k-means (partition.py:149-150): f64
+// centroids, same tensor-core pass + exact f64 decision, ties to the lower list.
+extern "C" int ivftq_assign_tc64(const double* xn, const double* centroids, int64_t n,
+                                 int n_lists, int dim, int32_t* list_out, void* scratch,
+                                 size_t scratch_bytes, void* stream) {
+  if (n == 0) return 0;
+  if (!ivftq_coarse_tc_supported(dim, n_lists)) {
+    set_error("assign_tc64: shape not supported (dim %d)", dim);
+    return IVFTQ_ERR_UNSUPPORTED;
+  }
+  return assign_tc_t<double>(xn, centroids, n, n_lists, dim, list_out, scratch, scratch_bytes,
+                             stream);
 }
 
 extern "C" size_t ivftq_probe_tc_scratch_bytes(int64_t nq, int n_lists, int dim) {

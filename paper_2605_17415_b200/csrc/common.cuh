@@ -103,37 +103,39 @@ __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, 
 #endif
 
 template <typename Load>
-__device__ double pw_block(Load ld, int base, int n) {
+__device__ double pw_block_raw(Load ld, int base, int n) {
   if (n < 8) {
     double r = -0.0;
-    for (int i = 0; i < n; ++i) r = add(r, sq(ld(base + i)));
+    for (int i = 0; i < n; ++i) r = add(r, (ld(base + i)));
     return r;
   }
-  double r0 = sq(ld(base + 0)), r1 = sq(ld(base + 1)), r2 = sq(ld(base + 2)),
-         r3 = sq(ld(base + 3)), r4 = sq(ld(base + 4)), r5 = sq(ld(base + 5)),
-         r6 = sq(ld(base + 6)), r7 = sq(ld(base + 7));
+  double r0 = (ld(base + 0)), r1 = (ld(base + 1)), r2 = (ld(base + 2)),
+         r3 = (ld(base + 3)), r4 = (ld(base + 4)), r5 = (ld(base + 5)),
+         r6 = (ld(base + 6)), r7 = (ld(base + 7));
   int i = 8;
   int lim = n - (n % 8);
   for (; i < lim; i += 8) {
-    r0 = add(r0, sq(ld(base + i + 0)));
-    r1 = add(r1, sq(ld(base + i + 1)));
-    r2 = add(r2, sq(ld(base + i + 2)));
-    r3 = add(r3, sq(ld(base + i + 3)));
-    r4 = add(r4, sq(ld(base + i + 4)));
-    r5 = add(r5, sq(ld(base + i + 5)));
-    r6 = add(r6, sq(ld(base + i + 6)));
-    r7 = add(r7, sq(ld(base + i + 7)));
+    r0 = add(r0, (ld(base + i + 0)));
+    r1 = add(r1, (ld(base + i + 1)));
+    r2 = add(r2, (ld(base + i + 2)));
+    r3 = add(r3, (ld(base + i + 3)));
+    r4 = add(r4, (ld(base + i + 4)));
+    r5 = add(r5, (ld(base + i + 5)));
+    r6 = add(r6, (ld(base + i + 6)));
+    r7 = add(r7, (ld(base + i + 7)));
   }
   double res = add(add(add(r0, r1), add(r2, r3)), add(add(r4, r5), add(r6, r7)));
-  for (; i < n; ++i) res = add(res, sq(ld(base + i)));
+  for (; i < n; ++i) res = add(res, (ld(base + i)));
   return res;
 }
 
 // Iterative form of numpy's recursion: split n > 128 at n2 = n/2 - (n/2 % 8)
 // and add the halves' sums left + right. Depth <= 16 for any int length.
+// numpy's pairwise sum of ld(0..n) (np.add.reduce along a strided or
+// contiguous axis, loops_utils.h.src pairwise_sum)
 template <typename Load>
-__device__ double pw_sumsq(Load ld, int n) {
-  if (n <= kPwBlock) return pw_block(ld, 0, n);
+__device__ double pw_sum(Load ld, int n) {
+  if (n <= kPwBlock) return pw_block_raw(ld, 0, n);
   // explicit post-order traversal
   int st_base[24], st_n[24];
   double st_left[24];
@@ -144,7 +146,7 @@ __device__ double pw_sumsq(Load ld, int n) {
   while (sp >= 0) {
     int b = st_base[sp], m = st_n[sp];
     if (m <= kPwBlock) {
-      ret = pw_block(ld, b, m);
+      ret = pw_block_raw(ld, b, m);
       --sp;
       // deliver to parent
       while (sp >= 0) {
@@ -171,6 +173,12 @@ __device__ double pw_sumsq(Load ld, int n) {
     st_base[sp] = b; st_n[sp] = h; st_state[sp] = 0;
   }
   return ret;
+}
+
+// ... and of the squares (np.linalg.norm's sum of squares)
+template <typename Load>
+__device__ double pw_sumsq(Load ld, int n) {
+  return pw_sum([&](int i) { return sq(ld(i)); }, n);
 }
 
 // The same sum for one row in shared memory, computed by the 8 lanes of an

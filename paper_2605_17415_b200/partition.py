@@ -164,15 +164,27 @@ def train_partition(data: np.ndarray, n_lists: int, seed: int, max_iters: int = 
                            lists=lists)
 
 
-def _train_device(data: np.ndarray, n_lists: int, seed_value: int, max_iters: int,
-                  chunk: int = 1 << 16) -> CoarsePartition:
-    """The same algorithm and RNG call sequence as the host path, with the data
-    resident on the GPU: f64 products through ivftq_gemm_nt, the n-long
-    k-means++ potential and Lloyd sums kept on the device (sums by a
-    deterministic segmented reduction over rows sorted by list). Only the
-    sampling vector p (8n bytes per seeding step) and a few scalars cross to
-    the host. Results differ from the host path only through f64 summation
-    order; memory is O(n*d + chunk*L), so it trains 1M x 4096 in one pass.
+def _train_device(data: np.ndarray, n_lists: int, seed_value: int, max_iters: int) -> CoarsePartition:
+    """The same algorithm and RNG call sequence as the host path, as hand-written
+    kernels over device-resident rows (csrc/kmeans.cu, csrc/coarse_tc.cu):
+
+    * k-means++ seeding (partition.py:83-113): `ivftq_kmeanspp_seed` runs all
+      k steps on the device from the host's uniforms (drawn up front: the
+      generator yields the same stream as k-1 calls of rng.random(nc));
+    * Lloyd assignment (partition.py:149-150): `ivftq_assign_tc64`, the
+      tensor-core pass with the exact f64 guard band on the step's f64
+      centroids, ties to the lower list;
+    * Lloyd update (partition.py:153-170): `ivftq_kmeans_sums` (stable
+      counting sort + in-order f64 sums, bit-identical to np.add.reduceat)
+      and `ivftq_normalize_rows` (numpy's pairwise norm, then the division).
+
+    One small read-back per Lloyd step (converged / empty list / zero sum).
+    Differences from the host path: the seeding's cdf and candidate scores
+    and the assignment's exact scores use a fixed f64 summation order that
+    is not OpenBLAS's, so a sample or an arg-max can differ where two values
+    agree to the last ulps; everything else is bit-identical. The rare
+    branches (fewer distinct points than k, empty lists, zero sums) follow
+    the reference through torch glue.
     """
     import torch
 
@@ -185,95 +197,130 @@ def _train_device(data: np.ndarray, n_lists: int, seed_value: int, max_iters: in
     n, dim = X.shape
     k = n_lists
     rng = np.random.default_rng(seed_value)
+    sp = _lib.stream_ptr
+
+    if not L.ivftq_coarse_tc_supported(dim, k):
+        raise ValueError(f"device k-means needs a padded dim <= 256, got dim={dim}")
 
     def gemm(A, B):
         out = torch.empty((A.shape[0], B.shape[0]), dtype=f64, device=dev)
         _lib.check(L.ivftq_gemm_nt(A.data_ptr(), B.data_ptr(), _lib.IVFTQ_F64, A.shape[0],
-                                   B.shape[0], dim, out.data_ptr(), _lib.IVFTQ_F64,
-                                   _lib.stream_ptr()), "gemm_nt")
+                                   B.shape[0], dim, out.data_ptr(), _lib.IVFTQ_F64, sp()), "gemm_nt")
         return out
 
-    def argmax_ip(C):
-        a = torch.empty(n, dtype=torch.int64, device=dev)
-        best = torch.empty(n, dtype=f64, device=dev)
-        for s0 in range(0, n, chunk):
-            v, i = gemm(X[s0:s0 + chunk], C).max(dim=1)  # first maximal index on ties
-            a[s0:s0 + chunk] = i
-            best[s0:s0 + chunk] = v
-        return a, best
-
-    def dist2(rows):
-        return torch.clamp(2.0 - 2.0 * gemm(X, X[torch.as_tensor(rows, device=dev)]), min=0.0)
-
-    # ---- k-means++ seeding (partition.py:_kmeanspp) ----
-    # rng.choice(n, size=nc, p=p) draws rng.random(nc) and searches the
-    # normalised cdf of p (side="right"); here the host draws the same
-    # uniforms and the cdf / search / potential / argmin stay on the device.
-    # The fast pass never synchronises; it records each step's potential
-    # total, and a degenerate step (total <= eps: fewer distinct points than
-    # k) re-runs the seeding with the host-checked branch of the reference.
-    nc = 2 + int(np.log2(k)) if k > 1 else 1
-
-    def seed(rng, checked):
-        chosen = torch.empty(k, dtype=torch.int64, device=dev)
-        tots = torch.empty(k, dtype=f64, device=dev)
-        c0 = int(rng.integers(n))
-        chosen[0] = c0
-        d2 = dist2([c0])[:, 0].contiguous()
-        for j in range(1, k):
-            tot = d2.sum()
-            tots[j] = tot
-            if checked and float(tot.item()) <= _EPS:
-                keep = np.ones(n, dtype=bool)
-                keep[chosen[:j].cpu().numpy()] = False
-                pool = np.flatnonzero(keep)
-                cj = int(rng.choice(pool)) if len(pool) else int(rng.integers(n))
-                chosen[j] = cj
-                d2 = torch.minimum(d2, dist2([cj])[:, 0])
-                continue
-            cdf = torch.cumsum(d2 / tot, 0)
-            cdf /= cdf[-1].clone()
-            u = torch.from_numpy(rng.random(nc)).to(dev, non_blocking=True)
-            cand = torch.clamp(torch.searchsorted(cdf, u, right=True), max=n - 1)
-            cd2 = torch.clamp(2.0 - 2.0 * gemm(X, X[cand]), min=0.0)
-            pot = torch.minimum(d2[:, None], cd2).sum(dim=0)
-            bsel = torch.argmin(pot)  # first minimal index, like np.argmin
-            chosen[j] = cand[bsel]
-            d2 = torch.minimum(d2, cd2.index_select(1, bsel.reshape(1))[:, 0]).contiguous()
-        return chosen, k == 1 or float(tots[1:].min().item()) > _EPS
-
-    chosen, ok = seed(rng, checked=False)
-    if not ok:
+    # ---- k-means++ seeding ----
+    nc = int(L.ivftq_kmeanspp_candidates(k))
+    first = int(rng.integers(n))
+    uniforms = np.ascontiguousarray(rng.random((max(k - 1, 0), nc)))
+    chosen = torch.empty(k, dtype=torch.int64, device=dev)
+    tots = torch.empty(k, dtype=f64, device=dev)
+    nbytes = int(L.ivftq_kmeanspp_scratch_bytes(n, dim, k))
+    scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    _lib.check(L.ivftq_kmeanspp_seed(X.data_ptr(), n, dim, k, first,
+                                     uniforms.ctypes.data if k > 1 else None, chosen.data_ptr(),
+                                     tots.data_ptr(), scratch.data_ptr(), nbytes, sp()),
+               "kmeanspp_seed")
+    del scratch
+    if k > 1 and float(tots[1:].min().item()) <= _EPS:
+        # fewer distinct points than k: the reference's checked branch
+        # (partition.py:91-98), replayed from the seed with host decisions
         rng = np.random.default_rng(seed_value)
-        chosen, _ = seed(rng, checked=True)
+        chosen = _seed_checked(X, k, nc, rng, gemm)
     cent = X[chosen].clone()
 
-    # ---- Lloyd iterations (partition.py:147-170) ----
-    prev = None
+    # ---- Lloyd iterations ----
+    abytes = int(L.ivftq_assign_tc_scratch_bytes(n, k, dim))
+    sbytes = int(L.ivftq_kmeans_sums_scratch_bytes(n, k))
+    scratch = torch.empty(max(abytes, sbytes), dtype=torch.uint8, device=dev)
+    a = torch.empty(n, dtype=torch.int32, device=dev)
+    prev = torch.empty(n, dtype=torch.int32, device=dev)
+    sums = torch.empty((k, dim), dtype=f64, device=dev)
+    cnt = torch.empty(k, dtype=torch.int32, device=dev)
+    flags = torch.zeros(2, dtype=torch.int64, device=dev)  # [assignments differ, first zero-norm sum]
+    differ = torch.zeros(1, dtype=torch.int32, device=dev)
+
+    def assign_into(out):
+        _lib.check(L.ivftq_assign_tc64(X.data_ptr(), cent.data_ptr(), n, k, dim, out.data_ptr(),
+                                       scratch.data_ptr(), scratch.numel(), sp()), "assign_tc64")
+
+    have_prev = False
     for _ in range(max_iters):
-        a, best = argmax_ip(cent)
-        if prev is not None and torch.equal(a, prev):
-            break
-        prev = a
-        cnt = torch.bincount(a, minlength=k)
-        order = torch.argsort(a, stable=True)
-        sums = torch.segment_reduce(X[order], "sum", lengths=cnt, axis=0)
-        cnt_h = cnt.cpu().numpy()
-        empty = np.flatnonzero(cnt_h == 0)
-        if len(empty):
-            far = torch.argsort(best, stable=True)[: len(empty)]
-            sums[torch.as_tensor(empty, device=dev)] = X[far]
-        nn = torch.linalg.vector_norm(sums, dim=1)
-        bad = np.flatnonzero((nn < _EPS).cpu().numpy())
-        if len(bad):
-            for slot in bad:
-                sums[int(slot)] = X[int(rng.integers(n))]
+        assign_into(a)
+        if have_prev:
+            _lib.check(L.ivftq_lists_differ(a.data_ptr(), prev.data_ptr(), n, differ.data_ptr(), sp()),
+                       "lists_differ")
+            if int(differ.item()) == 0:
+                break
+        prev.copy_(a)
+        have_prev = True
+        _lib.check(L.ivftq_kmeans_sums(X.data_ptr(), a.data_ptr(), n, dim, k, sums.data_ptr(),
+                                       cnt.data_ptr(), scratch.data_ptr(), scratch.numel(), sp()),
+                   "kmeans_sums")
+        new_cent = torch.empty_like(sums)
+        _lib.check(L.ivftq_normalize_rows(sums.data_ptr(), _lib.IVFTQ_F64, k, dim,
+                                          new_cent.data_ptr(), flags[1:].data_ptr(), sp()),
+                   "normalize_rows")
+        flags[0] = cnt.amin()
+        min_cnt, bad_row = (int(v) for v in flags.cpu())
+        if min_cnt == 0 or bad_row < k:
+            # rare branches of partition.py:161-170, in the reference's order
+            cnt_h = cnt.cpu().numpy()
+            empty = np.flatnonzero(cnt_h == 0)
+            if len(empty):
+                best = torch.empty(n, dtype=f64, device=dev)
+                _lib.check(L.ivftq_rowdot64(X.data_ptr(), cent.data_ptr(), a.data_ptr(), n, dim,
+                                          best.data_ptr(), sp()), "rowdot")
+                far = torch.argsort(best, stable=True)[: len(empty)]
+                sums[torch.as_tensor(empty, device=dev)] = X[far]
             nn = torch.linalg.vector_norm(sums, dim=1)
-        cent = sums / nn[:, None]
-    final, _ = argmax_ip(cent)
-    final = final.cpu().numpy()
+            for slot in np.flatnonzero((nn < _EPS).cpu().numpy()):
+                sums[int(slot)] = X[int(rng.integers(n))]
+            _lib.check(L.ivftq_normalize_rows(sums.data_ptr(), _lib.IVFTQ_F64, k, dim,
+                                              new_cent.data_ptr(), flags[1:].data_ptr(), sp()),
+                       "normalize_rows")
+        cent = new_cent
+    assign_into(a)
+    final = a.cpu().numpy().astype(np.int64)
     order = np.argsort(final, kind="stable")
     counts = np.bincount(final, minlength=k)
     lists = [m.tolist() for m in np.split(order, np.cumsum(counts)[:-1])]
     return CoarsePartition(n_lists=k, dim=dim, centroids=cent.cpu().numpy().astype(np.float32),
                            lists=lists)
+
+
+def _seed_checked(X, k, nc, rng, gemm):
+    """partition.py:_kmeanspp with the degenerate branch (total potential <= eps)
+    decided on the host each step; only reached when the data hold fewer
+    distinct points than k."""
+    import torch
+
+    dev = X.device
+    n = X.shape[0]
+
+    def dist2(rows):
+        return torch.clamp(2.0 - 2.0 * gemm(X, X[torch.as_tensor(rows, device=dev)]), min=0.0)
+
+    chosen = torch.empty(k, dtype=torch.int64, device=dev)
+    c0 = int(rng.integers(n))
+    chosen[0] = c0
+    d2 = dist2([c0])[:, 0].contiguous()
+    for j in range(1, k):
+        tot = d2.sum()
+        if float(tot.item()) <= _EPS:
+            keep = np.ones(n, dtype=bool)
+            keep[chosen[:j].cpu().numpy()] = False
+            pool = np.flatnonzero(keep)
+            cj = int(rng.choice(pool)) if len(pool) else int(rng.integers(n))
+            chosen[j] = cj
+            d2 = torch.minimum(d2, dist2([cj])[:, 0])
+            continue
+        cdf = torch.cumsum(d2 / tot, 0)
+        cdf /= cdf[-1].clone()
+        u = torch.from_numpy(rng.random(nc)).to(dev)
+        cand = torch.clamp(torch.searchsorted(cdf, u, right=True), max=n - 1)
+        cd2 = torch.clamp(2.0 - 2.0 * gemm(X, X[cand]), min=0.0)
+        pot = torch.minimum(d2[:, None], cd2).sum(dim=0)
+        bsel = torch.argmin(pot)
+        chosen[j] = cand[bsel]
+        d2 = torch.minimum(d2, cd2.index_select(1, bsel.reshape(1))[:, 0]).contiguous()
+    return chosen

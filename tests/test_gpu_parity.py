@@ -429,17 +429,112 @@ class TestRefresh:
 
 @pytest.mark.parametrize("name", ["d32_b4_L16_raw", "d128_b4_L64", "d200_b3_L16"])
 def test_train_partition_device_matches_reference(golden, name):
-    """GPU k-means (same algorithm and RNG sequence, f64 products on the device)
-    against the reference's centroids: identical up to f64 summation order."""
+    """GPU k-means (csrc/kmeans.cu: seeding, tensor-core Lloyd assignment,
+    in-order Lloyd sums) against the reference's own centroids
+    (partition.py:64-178). The Lloyd sums and the normalisation are
+    bit-identical by construction; the seeding's cdf / candidate scores and
+    the exact assignment scores use a fixed summation order that is not
+    OpenBLAS's, which can move a centroid by ulps of f64 before the f32 cast:
+    the f32 centroids must agree to one f32 ulp, the memberships exactly."""
     from paper_2605_17415_b200.partition import train_partition
 
     g = golden(name)
     x = g["x"].astype(np.float64)
     xn = x / np.linalg.norm(x, axis=1)[:, None]
-    p = train_partition(xn, int(g["config"][2]), seed=int(g["config"][7]), device="cuda")
-    np.testing.assert_allclose(p.centroids, g["centroids"], rtol=0, atol=1e-6)
-    sizes = np.array([len(m) for m in p.lists])
-    assert sizes.sum() == len(x)
+    L = int(g["config"][2])
+    p = train_partition(xn, L, seed=int(g["config"][7]), device="cuda")
+    np.testing.assert_allclose(p.centroids, g["centroids"], rtol=0, atol=2.0 ** -23)
+    h = train_partition(xn, L, seed=int(g["config"][7]), device="cpu")
+    assert [sorted(m) for m in p.lists] == [sorted(m) for m in h.lists]
+
+
+def test_kmeans_sums_bit_identical_to_reduceat():
+    """ivftq_kmeans_sums == np.add.reduceat over the stably sorted rows
+    (partition.py:153-158), bit for bit, with empty lists and one long list."""
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+
+    L = _lib.lib()
+    rng = np.random.default_rng(5)
+    for n, d, k in [(5000, 24, 37), (70000, 96, 512), (300, 200, 4)]:
+        x = rng.standard_normal((n, d))
+        a = rng.integers(0, k, n).astype(np.int32)
+        a[a == 3] = 2                      # list 3 empty
+        a[: n // 3] = 1                    # one long list
+        cnt = np.bincount(a, minlength=k)
+        order = np.argsort(a, kind="stable")
+        starts = np.concatenate(([0], np.cumsum(cnt)[:-1]))
+        ne = np.flatnonzero(cnt > 0)
+        want = np.zeros((k, d))
+        want[ne] = np.add.reduceat(x[order], starts[ne], axis=0)
+        X = torch.from_numpy(x).cuda()
+        A = torch.from_numpy(a).cuda()
+        sums = torch.empty((k, d), dtype=torch.float64, device="cuda")
+        counts = torch.empty(k, dtype=torch.int32, device="cuda")
+        nb = int(L.ivftq_kmeans_sums_scratch_bytes(n, k))
+        scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        _lib.check(L.ivftq_kmeans_sums(X.data_ptr(), A.data_ptr(), n, d, k, sums.data_ptr(),
+                                       counts.data_ptr(), scratch.data_ptr(), nb, _lib.stream_ptr()))
+        assert np.array_equal(counts.cpu().numpy(), cnt)
+        assert np.array_equal(sums.cpu().numpy().view(np.uint64), want.view(np.uint64))
+
+
+@pytest.mark.parametrize("n,d,k", [(3000, 16, 8), (20000, 96, 64), (6000, 200, 33)])
+def test_kmeanspp_seed_matches_host(n, d, k):
+    """Device seeding picks the host's centres (partition.py:_kmeanspp) from
+    the same generator stream."""
+    import torch
+
+    from paper_2605_17415_b200 import _lib
+    from paper_2605_17415_b200.partition import _HostOps, _kmeanspp
+
+    L = _lib.lib()
+    rng = np.random.default_rng(n + k)
+    x = rng.standard_normal((n, d))
+    x /= np.linalg.norm(x, axis=1)[:, None]
+    want = _kmeanspp(x, k, np.random.default_rng(77), _HostOps())
+    g = np.random.default_rng(77)
+    nc = int(L.ivftq_kmeanspp_candidates(k))
+    assert nc == 2 + int(np.log2(k))
+    first = int(g.integers(n))
+    u = np.ascontiguousarray(g.random((k - 1, nc)))
+    X = torch.from_numpy(x).cuda()
+    chosen = torch.empty(k, dtype=torch.int64, device="cuda")
+    tots = torch.empty(k, dtype=torch.float64, device="cuda")
+    nb = int(L.ivftq_kmeanspp_scratch_bytes(n, d, k))
+    scratch = torch.empty(nb, dtype=torch.uint8, device="cuda")
+    _lib.check(L.ivftq_kmeanspp_seed(X.data_ptr(), n, d, k, first, u.ctypes.data, chosen.data_ptr(),
+                                     tots.data_ptr(), scratch.data_ptr(), nb, _lib.stream_ptr()))
+    got = x[chosen.cpu().numpy()]
+    assert np.array_equal(got, want)
+    assert float(tots[1:].min()) > 0
+
+
+def test_train_partition_device_degenerate_and_repeatable():
+    """Fewer distinct points than k takes the reference's checked seeding
+    branch (partition.py:91-98) and its empty-list rule (partition.py:161-165).
+    Which duplicate the rule re-seeds from hangs on the last ulp of equal
+    scores (OpenBLAS's order on the host), so the check is structural: every
+    centroid is one of the distinct points and each point keeps a list. Two
+    runs agree bit for bit."""
+    from paper_2605_17415_b200.partition import train_partition
+
+    rng = np.random.default_rng(3)
+    base = rng.standard_normal((6, 24))
+    base /= np.linalg.norm(base, axis=1)[:, None]
+    x = base[rng.integers(0, 6, 400)]
+    p = train_partition(x, 8, seed=4, device="cuda")
+    gap = np.abs(p.centroids[:, None, :].astype(np.float64) - base[None]).max(axis=2)
+    assert np.all(gap.min(axis=1) <= 2.0 ** -23)
+    assert set(gap.argmin(axis=1).tolist()) == set(range(6))
+    assert sum(len(m) for m in p.lists) == len(x)
+    y = rng.standard_normal((5000, 48))
+    y /= np.linalg.norm(y, axis=1)[:, None]
+    a = train_partition(y, 32, seed=9, device="cuda")
+    b = train_partition(y, 32, seed=9, device="cuda")
+    assert np.array_equal(a.centroids.view(np.uint32), b.centroids.view(np.uint32))
+    assert a.lists == b.lists
 
 
 def _coarse_case(seed, n, L, d, dup=True):
