@@ -127,43 +127,68 @@ kpp_search_kernel(const double* __restrict__ d2, const double* __restrict__ S, i
 
 // Scores of kCandRows rows against the nc candidate rows: cd2t[c][i] =
 // max(2 - 2 x_i.x_c, 0), and the block's part of each candidate's potential
-// sum_i min(d2[i], cd2[i][c]). Thread = 2 rows x NCH candidates.
+// sum_i min(d2[i], cd2[i][c]). Thread = 2 rows x NCH candidates; the rows
+// pass through shared memory kCandK coordinates at a time (several blocks per
+// SM: one block's loads overlap the others' DFMAs), the candidate rows sit
+// transposed ([k][candidate], 16-byte pairs) for the whole block.
+constexpr int kCandK = 32;
 template <int NCH>
 __global__ void __launch_bounds__(128)
 kpp_cand_kernel(const double* __restrict__ X, int64_t n, int d, const int64_t* __restrict__ cand,
                 int nc, const double* __restrict__ d2, int use_d2, double* __restrict__ cd2t,
                 double* __restrict__ potp) {
-  extern __shared__ double sm[];
-  const int ld = d | 1;  // odd row stride: conflict-free column walks
-  double* xs = sm;                              // kCandRows x ld
-  double* cs = xs + (size_t)kCandRows * (ld > 2 * NCH ? ld : 2 * NCH);  // 2 * NCH x d
-  double* part = xs;                            // kCandRows x 2 NCH, over the row tile once it is consumed
+  extern __shared__ __align__(16) double sm[];
+  constexpr int NCHP = (NCH + 1) & ~1, CW = 2 * NCHP;
+  constexpr int XLD = kCandK + 1;
+  constexpr int XS = kCandRows * (XLD > 2 * NCH ? XLD : 2 * NCH);
+  double* cs = sm;                  // d x CW
+  double* xs = sm + (((size_t)d * CW + 1) & ~(size_t)1);  // kCandRows x XLD
+  double* part = xs;                // kCandRows x 2 NCH once the rows are consumed
+  (void)XS;
   const int t = threadIdx.x;
   const int64_t row0 = (int64_t)blockIdx.x * kCandRows;
   const int rows = (int)((n - row0) < kCandRows ? (n - row0) : kCandRows);
-  for (int i = t; i < kCandRows * d; i += 128) {
-    const int r = i / d, k = i - r * d;
-    xs[r * ld + k] = r < rows ? X[(row0 + r) * d + k] : 0.0;
+  for (int i = t; i < d * CW; i += 128) {
+    const int k = i / CW, w = i - k * CW;
+    const int cg = w / NCHP, c = w - cg * NCHP;
+    const int cc = cg * NCH + c;
+    cs[i] = (c < NCH && cc < nc) ? X[cand[cc] * d + k] : 0.0;
   }
-  for (int i = t; i < 2 * NCH * d; i += 128) {
-    const int c = i / d, k = i - c * d;
-    cs[i] = c < nc ? X[cand[c] * d + k] : 0.0;
-  }
-  __syncthreads();
   const int rp = t & 63, cg = t >> 6;
-  double acc0[NCH], acc1[NCH];
+  double acc0[NCHP], acc1[NCHP];
 #pragma unroll
-  for (int c = 0; c < NCH; ++c) acc0[c] = acc1[c] = 0.0;
-  const double* x0 = xs + rp * ld;
-  const double* x1 = xs + (rp + 64) * ld;
-  const double* cb = cs + (size_t)cg * NCH * d;
-  for (int k = 0; k < d; ++k) {
-    const double a = x0[k], b = x1[k];
+  for (int c = 0; c < NCHP; ++c) acc0[c] = acc1[c] = 0.0;
+  const double* x0 = xs + rp * XLD;
+  const double* x1 = xs + (rp + 64) * XLD;
+  for (int k0 = 0; k0 < d; k0 += kCandK) {
+    __syncthreads();  // the previous chunk is consumed (and cs is written)
+    // asynchronous 8-byte copies: all of a thread's loads of the chunk in flight
+#pragma unroll 8
+    for (int i = t; i < kCandRows * kCandK; i += 128) {
+      const int r = i / kCandK, kk = i - r * kCandK;
+      if (r < rows && k0 + kk < d) {
+        const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&xs[r * XLD + kk]);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst),
+                     "l"(&X[(row0 + r) * d + k0 + kk])
+                     : "memory");
+      } else {
+        xs[r * XLD + kk] = 0.0;
+      }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    const int kc = d - k0 < kCandK ? d - k0 : kCandK;
+    const double2* cp = (const double2*)(cs + (size_t)k0 * CW + cg * NCHP);
+    for (int kk = 0; kk < kc; ++kk) {
+      const double a = x0[kk], b = x1[kk];
 #pragma unroll
-    for (int c = 0; c < NCH; ++c) {
-      const double cv = cb[c * d + k];
-      acc0[c] = __fma_rn(a, cv, acc0[c]);
-      acc1[c] = __fma_rn(b, cv, acc1[c]);
+      for (int c2 = 0; c2 < NCHP / 2; ++c2) {
+        const double2 cv = cp[(size_t)kk * (CW / 2) + c2];
+        acc0[2 * c2] = __fma_rn(a, cv.x, acc0[2 * c2]);
+        acc1[2 * c2] = __fma_rn(b, cv.x, acc1[2 * c2]);
+        acc0[2 * c2 + 1] = __fma_rn(a, cv.y, acc0[2 * c2 + 1]);
+        acc1[2 * c2 + 1] = __fma_rn(b, cv.y, acc1[2 * c2 + 1]);
+      }
     }
   }
   __syncthreads();  // the row tile is dead: its space takes the per-row parts
@@ -382,8 +407,9 @@ static SeedScratch seed_layout(void* base, int64_t n, int k, int nc) {
 template <int NCH>
 static int launch_cand(const double* X, int64_t n, int d, const int64_t* cand, int nc,
                        const double* d2, int use_d2, double* cd2t, double* potp, cudaStream_t s) {
-  const size_t tile = (size_t)kCandRows * ((d | 1) > 2 * NCH ? (d | 1) : 2 * NCH);
-  const size_t smem = sizeof(double) * (tile + (size_t)2 * NCH * d);
+  constexpr int NCHP = (NCH + 1) & ~1;
+  const size_t tile = (size_t)kCandRows * (kCandK + 1 > 2 * NCH ? kCandK + 1 : 2 * NCH);
+  const size_t smem = sizeof(double) * (tile + (((size_t)d * 2 * NCHP + 1) & ~(size_t)1));
   auto fn = kpp_cand_kernel<NCH>;
   if (int e = smem_opt_in_dev((const void*)fn, smem)) return e;
   const unsigned grid = (unsigned)((n + kCandRows - 1) / kCandRows);

@@ -109,24 +109,38 @@ def _kmeanspp(data, k, rng, ops):
     return data[chosen].copy()
 
 
-def train_partition(data: np.ndarray, n_lists: int, seed: int, max_iters: int = 25,
-                    device: str = "cpu") -> CoarsePartition:
+def train_partition(data, n_lists: int, seed: int, max_iters: int = 25,
+                    device: str = "cpu", memberships: bool = True) -> CoarsePartition:
     """Spherical k-means++ / Lloyd on unit rows; f32 centroids + memberships.
 
     Args:
-        device: "cpu" (bit-exact with the reference) or "cuda" (f64 GEMMs on
-            the GPU; differs only through f64 summation order).
+        data: (n, dim) unit rows; a numpy array, or with device="cuda" also a
+            CUDA f64 tensor (the refresh sample never leaves the device).
+        device: "cpu" (bit-exact with the reference) or "cuda" (the
+            hand-written device k-means, `_train_device`).
+        memberships: False skips the final assignment and the per-list id
+            lists (refresh re-assigns every vector itself, refresh.py:183-203).
     """
-    data = np.asarray(data, dtype=np.float64)
-    n, dim = data.shape
     if n_lists < 1:
         raise ValueError(f"n_lists must be >= 1, got {n_lists}")
+    if not isinstance(data, np.ndarray) and hasattr(data, "is_cuda"):
+        import torch
+
+        if device != "cuda":
+            raise ValueError("a device tensor needs device='cuda'")
+        if data.shape[0] < n_lists:
+            raise ValueError(f"need at least n_lists={n_lists} rows, got {data.shape[0]}")
+        if bool((torch.linalg.vector_norm(data, dim=1) < _EPS).any()):
+            raise ValueError("zero-norm row in training data")
+        return _train_device(data, n_lists, seed, max_iters, memberships)
+    data = np.asarray(data, dtype=np.float64)
+    n, dim = data.shape
     if n < n_lists:
         raise ValueError(f"need at least n_lists={n_lists} rows, got {n}")
     if np.any(np.linalg.norm(data, axis=1) < _EPS):
         raise ValueError("zero-norm row in training data")
     if device == "cuda":
-        return _train_device(data, n_lists, seed, max_iters)
+        return _train_device(data, n_lists, seed, max_iters, memberships)
     ops = _HostOps()
     rng = np.random.default_rng(seed)
     cent = _kmeanspp(data, n_lists, rng, ops)
@@ -164,7 +178,8 @@ def train_partition(data: np.ndarray, n_lists: int, seed: int, max_iters: int = 
                            lists=lists)
 
 
-def _train_device(data: np.ndarray, n_lists: int, seed_value: int, max_iters: int) -> CoarsePartition:
+def _train_device(data, n_lists: int, seed_value: int, max_iters: int,
+                  memberships: bool = True) -> CoarsePartition:
     """The same algorithm and RNG call sequence as the host path, as hand-written
     kernels over device-resident rows (csrc/kmeans.cu, csrc/coarse_tc.cu):
 
@@ -193,7 +208,10 @@ def _train_device(data: np.ndarray, n_lists: int, seed_value: int, max_iters: in
     L = _lib.lib()
     dev = torch.device("cuda", torch.cuda.current_device())
     f64 = torch.float64
-    X = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dev)
+    if isinstance(data, np.ndarray):
+        X = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(dev)
+    else:
+        X = data.to(device=dev, dtype=f64).contiguous()
     n, dim = X.shape
     k = n_lists
     rng = np.random.default_rng(seed_value)
@@ -279,13 +297,15 @@ def _train_device(data: np.ndarray, n_lists: int, seed_value: int, max_iters: in
                                               new_cent.data_ptr(), flags[1:].data_ptr(), sp()),
                        "normalize_rows")
         cent = new_cent
+    cent32 = cent.cpu().numpy().astype(np.float32)
+    if not memberships:
+        return CoarsePartition(n_lists=k, dim=dim, centroids=cent32)
     assign_into(a)
     final = a.cpu().numpy().astype(np.int64)
     order = np.argsort(final, kind="stable")
     counts = np.bincount(final, minlength=k)
     lists = [m.tolist() for m in np.split(order, np.cumsum(counts)[:-1])]
-    return CoarsePartition(n_lists=k, dim=dim, centroids=cent.cpu().numpy().astype(np.float32),
-                           lists=lists)
+    return CoarsePartition(n_lists=k, dim=dim, centroids=cent32, lists=lists)
 
 
 def _seed_checked(X, k, nc, rng, gemm):

@@ -126,12 +126,21 @@ def _mean_rowdot(index, src: torch.Tensor, cent: torch.Tensor, lids: torch.Tenso
     return out[:n]
 
 
-def refresh(index: IvfTqIndex, policy: RefreshPolicy, kmeans_device: str = "cpu",
+# sample rows x lists above which "auto" trains on the device: the host path
+# materialises an (n, L) f64 score matrix per Lloyd step (2^27 entries = 1 GiB)
+_AUTO_DEVICE_WORK = 1 << 27
+
+
+def refresh(index: IvfTqIndex, policy: RefreshPolicy, kmeans_device: str = "auto",
             centroids: np.ndarray | None = None) -> RefreshReport:
     """Re-cluster the coarse partition and re-encode every vector on the GPU.
 
     Args:
-        kmeans_device: "cpu" (reference-exact k-means) or "cuda".
+        kmeans_device: "cpu" (numpy k-means, bit-exact with the reference's
+            OpenBLAS path), "cuda" (the hand-written device k-means,
+            partition.py:_train_device) or "auto": the device once the sample
+            times the list count reaches 2^27 (where the host path's per-step
+            (n, L) f64 score matrix passes 1 GiB), the host below that.
         centroids: inject pre-trained (L, d) f32 centroids instead of training
             (isolates the re-encode kernel in parity runs).
     """
@@ -152,7 +161,7 @@ def refresh(index: IvfTqIndex, policy: RefreshPolicy, kmeans_device: str = "cpu"
     # per-list members in ascending id order (what partition.lists holds,
     # refresh.py:115-121), as arrays: no Python list of n ints at 10M scale
     lids = index.list_ids
-    order = np.argsort(lids, kind="stable")
+    order = torch.argsort(index._list_of.t[:n], stable=True).cpu().numpy()  # = np.argsort(lids, "stable")
     members = np.split(order, np.cumsum(np.bincount(lids, minlength=n_lists))[:-1])
     sample_ids = _stratified_sample_ids(members, n, n_lists, sample_size, rng)
     dev = index.device
@@ -163,9 +172,17 @@ def refresh(index: IvfTqIndex, policy: RefreshPolicy, kmeans_device: str = "cpu"
             e = min(n, s + _CHUNK)
             sel = sid[(sid >= s) & (sid < e)] - s
             if sel.numel():
-                rows.append(_source_rows(index, used_raw, s, e)[sel].cpu().numpy())
-        sample = np.concatenate(rows)
-        new_part = train_partition(sample, n_lists, seed=policy.seed, device=kmeans_device)
+                rows.append(_source_rows(index, used_raw, s, e)[sel])
+        sample = torch.cat(rows)
+        del rows
+        if kmeans_device == "auto":
+            big = len(sample) * n_lists >= _AUTO_DEVICE_WORK
+            kmeans_device = "cuda" if big and (index.config.dim + 31) // 32 * 32 <= 256 else "cpu"
+        if kmeans_device != "cuda":
+            sample = sample.cpu().numpy()
+        new_part = train_partition(sample, n_lists, seed=policy.seed, device=kmeans_device,
+                                   memberships=False)
+        del sample
     else:
         from .partition import CoarsePartition
         new_part = CoarsePartition(n_lists, index.config.dim, np.asarray(centroids, np.float32))
