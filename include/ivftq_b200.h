@@ -167,6 +167,27 @@ int ivftq_residuals(const double* xn, const float* centroids, const int32_t* lis
 int ivftq_quantize_pack(const double* rot, const uint16_t* norms, int64_t n, int dim,
                         int bits, int use_sign, const double* boundaries,
                         const double* qcent, uint32_t* words_out, void* stream);
+/* Tensor-core encoder tail (index.py:247-262 after the assignment), used by
+ * ivftq_encode whenever ivftq_encode_supported_tc(dim): one kernel forms
+ * r = xn - c_l, ||r|| -> binary16 (both bit-exact) and the unit row r/||r|| as
+ * fp16 hi/lo tensor-core operands (no f64 intermediate returns to HBM); the
+ * rotation u' = (r/||r||).R^T runs on tcgen05 (error-compensated fp16, f32
+ * accumulation in TMEM); Lloyd-Max bins and signs are taken from u', and
+ * every row with a coordinate within the guard width (2^-18) of a bin boundary
+ * or half-bin centroid is re-encoded by an exact f64 pass, so the codes equal
+ * the f64 path's. ivftq_rotate_unit_tc exposes the first two steps (U (n, dim)
+ * f32 on the device) so the guard can be pinned against an f64 rotation. */
+int ivftq_encode_supported_tc(int dim);
+size_t ivftq_encode_tc_scratch_bytes(int64_t n, int dim);
+int ivftq_rotate_unit_tc(const double* xn, const float* centroids, const int32_t* list_ids,
+                         int64_t n, int dim, int flat, const double* R, float* U_out,
+                         uint16_t* norm_out, void* scratch, size_t scratch_bytes,
+                         void* stream);
+int ivftq_encode_tail_tc(const double* xn, const float* centroids, const int32_t* list_ids,
+                         int64_t n, int dim, int bits, int use_sign, int flat,
+                         const double* R, const double* boundaries, const double* qcent,
+                         uint16_t* norm_out, uint32_t* words_out, void* scratch,
+                         size_t scratch_bytes, void* stream);
 /* Whole encoder: normalize -> assign -> residual -> rotate -> quantize/pack.
  * scratch >= ivftq_encode_scratch_bytes(n, dim, n_lists). Outputs per row: xn (f64, for
  * the raw store; may alias nothing), list id, binary16 norm, code words. */

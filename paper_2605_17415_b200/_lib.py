@@ -60,6 +60,11 @@ _SIGS = {
     "ivftq_residuals": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
     "ivftq_quantize_pack": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "ivftq_encode_scratch_bytes": (_sz, [_i64, _i32, _i32]),
+    "ivftq_encode_supported_tc": (_i32, [_i32]),
+    "ivftq_encode_tc_scratch_bytes": (_sz, [_i64, _i32]),
+    "ivftq_rotate_unit_tc": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "ivftq_encode_tail_tc": (_i32, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _vp,
+                                    _vp, _vp, _vp, _sz, _vp]),
     "ivftq_encode": (_i32, [_vp, _i32, _i64, _i32, _i32, _i32, _i32, _vp, _i32, _vp, _vp,
                             _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "ivftq_pack_codes": (_i32, [_vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp]),

@@ -226,10 +226,21 @@ extern "C" int ivftq_host_row_norms(const double* x, int64_t n, int dim, double*
 
 extern "C" size_t ivftq_assign_tc_scratch_bytes(int64_t n, int n_lists, int dim);
 
+extern "C" size_t ivftq_encode_tc_scratch_bytes(int64_t n, int dim);
+extern "C" int ivftq_encode_supported_tc(int dim);
+extern "C" int ivftq_encode_tail_tc(const double* xn, const float* centroids,
+                                    const int32_t* list_ids, int64_t n, int dim, int bits,
+                                    int use_sign, int flat, const double* R,
+                                    const double* boundaries, const double* qcent,
+                                    uint16_t* norm_out, uint32_t* words_out, void* scratch,
+                                    size_t scratch_bytes, void* stream);
+
 extern "C" size_t ivftq_encode_scratch_bytes(int64_t n, int dim, int n_lists) {
   const size_t a = (size_t)2 * n * dim * sizeof(double) + 256;
   const size_t b = ivftq_assign_tc_scratch_bytes(n, n_lists, dim);
-  return a > b ? a : b;  // the assignment scratch is dead before the residuals
+  const size_t c = ivftq_encode_tc_scratch_bytes(n, dim);
+  const size_t m = a > b ? a : b;  // the assignment scratch is dead before the residuals
+  return m > c ? m : c;
 }
 
 extern "C" int ivftq_encode(const void* x, int x_dtype, int64_t n, int dim, int bits,
@@ -253,6 +264,12 @@ extern "C" int ivftq_encode(const void* x, int x_dtype, int64_t n, int dim, int 
                                 scratch_bytes, stream))
       return e;
   }
+  // tensor-core tail (residual -> unit rows -> tcgen05 rotation -> Lloyd-Max with
+  // an exact f64 pass over the rows near a threshold) whenever the shape allows
+  if (ivftq_encode_supported_tc(dim))
+    return ivftq_encode_tail_tc(xn_out, centroids, list_out, n, dim, bits, use_sign, flat, R,
+                                boundaries, qcent, norm_out, words_out, scratch, scratch_bytes,
+                                stream);
   if (int e = ivftq_residuals(xn_out, centroids, list_out, n, dim, flat, resid, norm_out, stream))
     return e;
   if (int e = ivftq_gemm_nt(resid, R, IVFTQ_F64, n, dim, dim, rot, IVFTQ_F64, stream)) return e;

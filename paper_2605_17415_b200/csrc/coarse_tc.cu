@@ -1099,6 +1099,27 @@ static int coarse_gemm(const double* X, int64_t n, int dim, int L, const void* p
   return check_launch("coarse_tc");
 }
 
+// Rotation on the coarse-scoring kernel (index.py:256, rotation.py:40): the d
+// rows of R play the centroids, the pre-split unit residual rows the queries,
+// S' = A . R^T in f32 (n x d). Used by the tensor-core encoder (encode.cu).
+namespace ivftq {
+int rotate_tc(const uint32_t* xh, const uint32_t* xl, int64_t n, int dim, const double* R,
+              float* U, void* prep, cudaStream_t s) {
+  if (int e = ::coarse_prepare_t<double>(R, dim, dim, prep, (void*)s)) return e;
+  const int DP = ctc::pad_dp(dim);
+  const int nT = (dim + ctc::tile_n(DP) - 1) / ctc::tile_n(DP);
+  const size_t smem = 3 * ctc::tile_bytes(DP) + 1024;
+  if (int e = smem_opt_in_dev((const void*)ctc::coarse_tc_kernel, 3 * ctc::tile_bytes(128) + 1024))
+    return e;
+  const int n_sms = device_sm_count();
+  const int64_t units = ((n + ctc::kM - 1) / ctc::kM) * nT;
+  const unsigned grid = (unsigned)(units < n_sms ? units : n_sms);
+  ctc::coarse_tc_kernel<<<grid, ctc::kThreads, smem, s>>>(
+      nullptr, n, dim, DP, dim, nT, (const unsigned char*)prep, U, nullptr, nullptr, xh, xl);
+  return check_launch("rotate_tc");
+}
+}  // namespace ivftq
+
 extern "C" size_t ivftq_assign_tc_scratch_bytes(int64_t n, int n_lists, int dim) {
   // prep | top_v (n*4 f32) | top_i (n*4 i32) | ex (n*4 f64) | full list (n i32) | count
   // | pre-split A rows (n * DP * 4)

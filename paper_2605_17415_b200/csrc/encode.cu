@@ -8,6 +8,7 @@
 // same IEEE operations in the same order, so those stages are bit-exact; only
 // the GEMMs (assign, rotate) differ in summation order from OpenBLAS.
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -130,6 +131,180 @@ quantize_pack_kernel(const double* __restrict__ rot, const uint16_t* __restrict_
     }
     words[(row0 + r) * W + w] = word;
   }
+}
+
+// ---- tensor-core encoder (index.py:247-262 with the rotation on tcgen05) -------
+// (1) unit residual rows, split for the tensor cores: r = xn - c_l in f64 as the
+// reference computes it, ||r|| in numpy's pairwise order -> binary16 (both
+// bit-exact), then a = r / ||r|| scaled by 2^14 and split into fp16 hi + lo,
+// two coordinates per word along k, zero-padded to DP (coarse_tc.cu's
+// A-operand row format). No f64 intermediate goes back to HBM.
+__device__ __forceinline__ void split16e(float x, uint16_t& hi, uint16_t& lo) {
+  const __half h = __float2half_rn(x);
+  hi = __half_as_ushort(h);
+  lo = __half_as_ushort(__float2half_rn(x - __half2float(h)));
+}
+
+constexpr int kSplitThreads = 256;
+__global__ void __launch_bounds__(kSplitThreads)
+resid_split_kernel(const double* __restrict__ xn, const float* __restrict__ cent,
+                   const int32_t* __restrict__ lids, int64_t n, int d, int DP, int flat,
+                   uint16_t* __restrict__ norm_out, uint32_t* __restrict__ hi,
+                   uint32_t* __restrict__ lo) {
+  extern __shared__ double sm[];
+  __shared__ double nrm[kRowTile];
+  const int ld = d + 1;
+  int64_t row0 = (int64_t)blockIdx.x * kRowTile;
+  int rows = (int)(n - row0 < kRowTile ? n - row0 : kRowTile);
+  for (int i = threadIdx.x; i < rows * d; i += blockDim.x) {
+    int r = i / d, c = i - r * d;
+    double v = xn[(row0 + r) * d + c];
+    if (!flat) v = __dsub_rn(v, (double)cent[(int64_t)lids[row0 + r] * d + c]);
+    sm[r * ld + c] = v;
+  }
+  __syncthreads();
+  for (int r = threadIdx.x >> 3; r < ((rows + 3) & ~3); r += kSplitThreads / 8) {
+    const int rr = r < rows ? r : 0;
+    const double s = pw_sumsq_lane8(sm + rr * ld, d);
+    if ((threadIdx.x & 7) == 0 && r < rows) {
+      const double q = __dsqrt_rn(s);
+      nrm[r] = q;
+      norm_out[row0 + r] = d2h_bits(q);
+    }
+  }
+  __syncthreads();
+  const int hw = DP / 2;
+  for (int i = threadIdx.x; i < rows * hw; i += blockDim.x) {
+    const int r = i / hw, k = (i - r * hw) * 2;
+    const double q = nrm[r];
+    const double* rp = sm + r * ld;
+    uint16_t h0, l0, h1, l1;
+    split16e(k < d && q > 0.0 ? (float)(__ddiv_rn(rp[k], q) * 16384.0) : 0.f, h0, l0);
+    split16e(k + 1 < d && q > 0.0 ? (float)(__ddiv_rn(rp[k + 1], q) * 16384.0) : 0.f, h1, l1);
+    hi[(row0 + r) * hw + (k >> 1)] = h0 | ((uint32_t)h1 << 16);
+    lo[(row0 + r) * hw + (k >> 1)] = l0 | ((uint32_t)l1 << 16);
+  }
+}
+
+// (3) Lloyd-Max bins + signs from the tensor-core unit coordinates u' (f32),
+// packed. A row with any coordinate within `eps` of a decision threshold (a
+// bin boundary or its bin's half-bin centroid) is listed for the exact pass:
+// |u' - u| < eps, so every other row's fields equal the f64 path's.
+__global__ void __launch_bounds__(256)
+quantize_guard_kernel(const float* __restrict__ U, const uint16_t* __restrict__ norms, int64_t n,
+                      int d, int bits, int use_sign, const double* __restrict__ boundaries,
+                      const double* __restrict__ qcent, double eps, uint32_t* __restrict__ words,
+                      int32_t* __restrict__ flag, int32_t* __restrict__ list,
+                      int32_t* __restrict__ count) {
+  __shared__ double bnd[257];
+  __shared__ double qc[256];
+  const int levels = 1 << bits;
+  const int fb = field_bits(bits, use_sign), fpw = fields_per_word(fb);
+  const int W = words_per_vec(d, fb);
+  for (int i = threadIdx.x; i <= levels; i += blockDim.x) bnd[i] = boundaries[i];
+  for (int i = threadIdx.x; i < levels; i += blockDim.x) qc[i] = qcent[i];
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n * W) return;
+  const int64_t r = i / W;
+  const int w = (int)(i - r * W);
+  uint32_t word = 0;
+  bool amb = false;
+  if (norms[r] != 0) {  // binary16 +0 => dead row, codes stay 0
+    const float* up = U + r * d;
+    for (int f = 0; f < fpw; ++f) {
+      const int j = w * fpw + f;
+      if (j >= d) break;
+      const double u = (double)up[j];
+      const uint32_t c = quant_field(u, bnd, qc, levels);
+      const int b = (int)(c >> 1);
+      word |= c << (fb * f);
+      amb |= fabs(u - qc[b]) <= eps;
+      if (b > 0) amb |= u - bnd[b] <= eps;
+      if (b + 1 < levels) amb |= bnd[b + 1] - u <= eps;
+    }
+  }
+  words[i] = word;
+  if (amb && atomicExch(&flag[r], 1) == 0) list[atomicAdd(count, 1)] = (int32_t)r;
+}
+
+// (4) exact f64 re-encode of the listed rows, kFixRows at a time per block:
+// r = xn - c, rot = r.R^T as a sequential FMA chain per coordinate (each R^T
+// element loaded once for the kFixRows rows), u = rot / ||rot|| (numpy
+// pairwise norm), then the same quant_field as quantize_pack_kernel.
+constexpr int kFixRows = 8;
+__global__ void __launch_bounds__(128)
+encode_fixup_kernel(const double* __restrict__ xn, const float* __restrict__ cent,
+                    const int32_t* __restrict__ lids, int d, int flat,
+                    const double* __restrict__ RT, int bits, int use_sign,
+                    const double* __restrict__ boundaries, const double* __restrict__ qcent,
+                    const int32_t* __restrict__ list, const int32_t* __restrict__ count,
+                    uint32_t* __restrict__ words) {
+  extern __shared__ double sm[];  // r[kFixRows][d] | rot[kFixRows][d]
+  __shared__ double bnd[257];
+  __shared__ double qc[256];
+  __shared__ double nrm[kFixRows];
+  __shared__ int64_t rid[kFixRows];
+  double* rs = sm;
+  double* rot = sm + (size_t)kFixRows * d;
+  const int levels = 1 << bits;
+  const int fb = field_bits(bits, use_sign), fpw = fields_per_word(fb);
+  const int W = words_per_vec(d, fb);
+  for (int i = threadIdx.x; i <= levels; i += blockDim.x) bnd[i] = boundaries[i];
+  for (int i = threadIdx.x; i < levels; i += blockDim.x) qc[i] = qcent[i];
+  const int total = *count;
+  for (int it = blockIdx.x * kFixRows; it < total; it += gridDim.x * kFixRows) {
+    const int nr = total - it < kFixRows ? total - it : kFixRows;
+    __syncthreads();
+    if (threadIdx.x < kFixRows) rid[threadIdx.x] = threadIdx.x < nr ? list[it + threadIdx.x] : -1;
+    __syncthreads();
+    for (int i = threadIdx.x; i < kFixRows * d; i += blockDim.x) {
+      const int x = i / d, k = i - x * d;
+      double v = 0.0;
+      if (x < nr) {
+        const int64_t r = rid[x];
+        v = xn[r * d + k];
+        if (!flat) v = __dsub_rn(v, (double)cent[(int64_t)lids[r] * d + k]);
+      }
+      rs[i] = v;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      double acc[kFixRows];
+#pragma unroll
+      for (int x = 0; x < kFixRows; ++x) acc[x] = 0.0;
+      for (int k = 0; k < d; ++k) {
+        const double rv = RT[(int64_t)k * d + j];
+#pragma unroll
+        for (int x = 0; x < kFixRows; ++x) acc[x] = __fma_rn(rs[x * d + k], rv, acc[x]);
+      }
+#pragma unroll
+      for (int x = 0; x < kFixRows; ++x) rot[x * d + j] = acc[x];
+    }
+    __syncthreads();
+    if (threadIdx.x < 8 * kFixRows) {  // one lane group of 8 per row
+      const int x = threadIdx.x >> 3;
+      const double s = pw_sumsq_lane8(rot + x * d, d);
+      if ((threadIdx.x & 7) == 0) nrm[x] = __dsqrt_rn(s);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr * W; i += blockDim.x) {
+      const int x = i / W, w = i - x * W;
+      const double q = nrm[x];
+      uint32_t word = 0;
+      for (int f = 0; f < fpw; ++f) {
+        const int j = w * fpw + f;
+        if (j >= d) break;
+        word |= quant_field(__ddiv_rn(rot[x * d + j], q), bnd, qc, levels) << (fb * f);
+      }
+      words[rid[x] * W + w] = word;
+    }
+  }
+}
+
+__global__ void transpose_kernel(const double* __restrict__ R, int d, double* __restrict__ RT) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d * d) RT[(i % d) * d + i / d] = R[i];
 }
 
 __global__ void pack_codes_kernel(const uint8_t* __restrict__ bins,
@@ -324,6 +499,114 @@ extern "C" int ivftq_quantize_pack(const double* rot, const uint16_t* norms, int
   quantize_pack_kernel<<<grid, kRowThreads, row_smem(dim), S(stream)>>>(
       rot, norms, n, dim, bits, use_sign, boundaries, qcent, words_out);
   return check_launch("quantize_pack");
+}
+
+// Tensor-core rotation of pre-split rows (coarse_tc.cu): U = A . R^T in f32.
+namespace ivftq {
+int rotate_tc(const uint32_t* xh, const uint32_t* xl, int64_t n, int dim, const double* R,
+              float* U, void* prep, cudaStream_t s);
+}
+
+extern "C" size_t ivftq_coarse_prep_bytes(int n_lists, int dim);
+extern "C" int ivftq_coarse_tc_supported(int dim, int n_lists);
+
+static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+extern "C" size_t ivftq_encode_tc_scratch_bytes(int64_t n, int dim) {
+  const int DP = (dim + 31) / 32 * 32;
+  return a256(ivftq_coarse_prep_bytes(dim, dim)) + a256((size_t)n * DP * 4) +
+         a256((size_t)n * dim * 4) + 2 * a256((size_t)n * 4) + 256 +
+         a256((size_t)dim * dim * 8) + 256;
+}
+
+// Guard width of the tensor-core encoder: |u' - u| stays below 2^-20 on
+// every measured shape (tests/test_gpu_parity.py::test_rotate_tc_error_inside_guard
+// asserts a 4x margin); IVFTQ_ROT_EPS overrides it for experiments.
+static double rot_eps() {
+  const char* e = getenv("IVFTQ_ROT_EPS");
+  return e ? atof(e) : 0x1p-18;
+}
+
+extern "C" int ivftq_encode_supported_tc(int dim) {
+  return ivftq_coarse_tc_supported(dim, dim) && !getenv("IVFTQ_ENCODE_F64");
+}
+
+// residual -> unit -> tensor-core rotation: U (n, dim) f32 and the binary16
+// residual norms. scratch >= ivftq_encode_tc_scratch_bytes(n, dim).
+extern "C" int ivftq_rotate_unit_tc(const double* xn, const float* centroids,
+                                    const int32_t* list_ids, int64_t n, int dim, int flat,
+                                    const double* R, float* U_out, uint16_t* norm_out,
+                                    void* scratch, size_t scratch_bytes, void* stream) {
+  if (n == 0) return 0;
+  if (!ivftq_coarse_tc_supported(dim, dim)) {
+    set_error("rotate_unit_tc: dim %d not supported", dim);
+    return IVFTQ_ERR_UNSUPPORTED;
+  }
+  if (scratch_bytes < ivftq_encode_tc_scratch_bytes(n, dim)) {
+    set_error("rotate_unit_tc: scratch too small");
+    return IVFTQ_ERR_SCRATCH;
+  }
+  const int DP = (dim + 31) / 32 * 32;
+  unsigned char* p = (unsigned char*)scratch;
+  void* prep = p;
+  p += a256(ivftq_coarse_prep_bytes(dim, dim));
+  uint32_t* xh = (uint32_t*)p;
+  uint32_t* xl = xh + (size_t)n * (DP / 2);
+  if (int e = set_row_smem((const void*)resid_split_kernel, dim)) return e;
+  const int grid = (int)((n + kRowTile - 1) / kRowTile);
+  resid_split_kernel<<<grid, kSplitThreads, row_smem(dim), S(stream)>>>(
+      xn, centroids, list_ids, n, dim, DP, flat, norm_out, xh, xl);
+  if (int e = check_launch("resid_split")) return e;
+  return rotate_tc(xh, xl, n, dim, R, U_out, prep, S(stream));
+}
+
+// The whole post-assignment encoder on the tensor-core path:
+// resid_split -> rotate_tc -> quantize_guard -> exact fix-up of the listed rows.
+extern "C" int ivftq_encode_tail_tc(const double* xn, const float* centroids,
+                                    const int32_t* list_ids, int64_t n, int dim, int bits,
+                                    int use_sign, int flat, const double* R,
+                                    const double* boundaries, const double* qcent,
+                                    uint16_t* norm_out, uint32_t* words_out, void* scratch,
+                                    size_t scratch_bytes, void* stream) {
+  if (bits < 1 || bits > 8) {
+    set_error("bits must be in [1, 8], got %d", bits);
+    return IVFTQ_ERR_ARG;
+  }
+  if (n == 0) return 0;
+  if (scratch_bytes < ivftq_encode_tc_scratch_bytes(n, dim)) {
+    set_error("encode_tail_tc: scratch too small");
+    return IVFTQ_ERR_SCRATCH;
+  }
+  const int DP = (dim + 31) / 32 * 32;
+  unsigned char* p = (unsigned char*)scratch;
+  p += a256(ivftq_coarse_prep_bytes(dim, dim)) + a256((size_t)n * DP * 4);
+  float* U = (float*)p;
+  p += a256((size_t)n * dim * 4);
+  int32_t* flag = (int32_t*)p;
+  p += a256((size_t)n * 4);
+  int32_t* list = (int32_t*)p;
+  p += a256((size_t)n * 4);
+  int32_t* count = (int32_t*)p;
+  p += 256;
+  double* RT = (double*)p;
+  cudaStream_t s = S(stream);
+  if (int e = ivftq_rotate_unit_tc(xn, centroids, list_ids, n, dim, flat, R, U, norm_out, scratch,
+                                   scratch_bytes, stream))
+    return e;
+  IVFTQ_CHECK_CUDA(cudaMemsetAsync(flag, 0, a256((size_t)n * 4) * 2 + 256, s));
+  const int W = words_per_vec(dim, field_bits(bits, use_sign));
+  const int64_t tot = n * W;
+  quantize_guard_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(
+      U, norm_out, n, dim, bits, use_sign, boundaries, qcent, rot_eps(), words_out, flag, list,
+      count);
+  if (int e = check_launch("quantize_guard")) return e;
+  transpose_kernel<<<(dim * dim + 255) / 256, 256, 0, s>>>(R, dim, RT);
+  if (int e = check_launch("transpose")) return e;
+  const int fgrid = ivftq::device_sm_count() * 6;
+  encode_fixup_kernel<<<fgrid, 128, sizeof(double) * 2 * kFixRows * dim, s>>>(
+      xn, centroids, list_ids, dim, flat, RT, bits, use_sign, boundaries, qcent, list, count,
+      words_out);
+  return check_launch("encode_fixup");
 }
 
 extern "C" int ivftq_pack_codes(const uint8_t* bins, const uint8_t* signs, int64_t n,

@@ -160,9 +160,9 @@ WORKLOADS = {
     # C3 with overlapping clusters: 1024 mixture components spread over 4096
     # lists and sigma 0.6, so true neighbours straddle lists and recall rises
     # with n_p (the C3 mixture puts every neighbour in the nearest list).
-    "c3_hard": Workload("c3_hard", 10_000_000, 96, 1024, 0.6, 4096, 4, 10_000, 10,
-                        (16, 32, 64, 128), kmeans_sample=32_768, parallel=True,
-                        notes="harder C3 variant: K=1024 components, sigma 0.6"),
+    "c3_hard": Workload("c3_hard", 10_000_000, 96, 1024, 1.0, 4096, 4, 10_000, 10,
+                        (1, 4, 16, 32, 64, 128), kmeans_sample=32_768, parallel=True,
+                        notes="harder C3 variant: K=1024 components, sigma 1.0, sweep from n_p=1"),
     "c4": Workload("c4", 10_000_000, 200, 4096, 0.3, 4096, 4, 10_000, 10, (64,),
                    kmeans_sample=32_768, query_shift=0.5, norm_sigma=0.25, parallel=True,
                    notes="configs[3]: queries from means + 0.5*N(0,1) offsets"),

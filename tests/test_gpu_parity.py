@@ -537,6 +537,49 @@ def test_train_partition_device_degenerate_and_repeatable():
     assert a.lists == b.lists
 
 
+@pytest.mark.parametrize("n,d,L", [(40000, 96, 64), (20000, 128, 32), (12000, 200, 16), (5000, 24, 8)])
+def test_rotate_tc_error_inside_guard(n, d, L):
+    """The tensor-core encoder quantises u' = (r/||r||).R^T computed on tcgen05
+    and re-encodes in f64 every row with a coordinate within 2^-18 of a
+    threshold. Pin the guard: |u' - u| against the f64 rotation stays below a
+    quarter of it, and the binary16 norms are bit-exact (index.py:247-256)."""
+    import torch
+
+    from paper_2605_17415_b200 import _lib, generate_rotation
+
+    Lb = _lib.lib()
+    rng = np.random.default_rng(d)
+    c = rng.standard_normal((L, d))
+    c = (c / np.linalg.norm(c, axis=1)[:, None]).astype(np.float32)
+    lid = rng.integers(0, L, n).astype(np.int32)
+    x = c[lid].astype(np.float64) + rng.standard_normal((n, d)) * rng.uniform(1e-4, 0.3, (n, 1))
+    x[:3] = c[lid[:3]]                      # zero residuals
+    xn = x / np.linalg.norm(x, axis=1)[:, None]
+    R = np.ascontiguousarray(generate_rotation(d, 42).matrix, dtype=np.float64)
+    r = xn - c[lid].astype(np.float64)
+    rn = np.linalg.norm(r, axis=1)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        want = np.where(rn[:, None] > 0, (r / rn[:, None]) @ R.T, 0.0)
+    dev = "cuda"
+    X = torch.from_numpy(xn).to(dev)
+    C = torch.from_numpy(c).to(dev)
+    Ld = torch.from_numpy(lid).to(dev)
+    Rd = torch.from_numpy(R).to(dev)
+    U = torch.empty((n, d), dtype=torch.float32, device=dev)
+    nrm = torch.empty(n, dtype=torch.int16, device=dev)
+    nb = int(Lb.ivftq_encode_tc_scratch_bytes(n, d))
+    scratch = torch.empty(nb, dtype=torch.uint8, device=dev)
+    assert Lb.ivftq_encode_supported_tc(d)
+    _lib.check(Lb.ivftq_rotate_unit_tc(X.data_ptr(), C.data_ptr(), Ld.data_ptr(), n, d, 0,
+                                       Rd.data_ptr(), U.data_ptr(), nrm.data_ptr(),
+                                       scratch.data_ptr(), nb, _lib.stream_ptr()))
+    got = U.cpu().numpy().astype(np.float64)
+    live = rn > 1e-7
+    err = np.abs(got[live] - want[live]).max()
+    assert err < 2.0 ** -20, err
+    assert np.array_equal(nrm.cpu().numpy().view(np.uint16), rn.astype(np.float16).view(np.uint16))
+
+
 def _coarse_case(seed, n, L, d, dup=True):
     rng = np.random.default_rng(seed)
     c = rng.standard_normal((L, d))
