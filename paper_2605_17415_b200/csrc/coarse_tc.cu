@@ -524,19 +524,29 @@ __global__ void assign_pick_kernel(int64_t n, const unsigned char* prep,
   out[r] = bi == INT_MAX ? 0 : bi;  // NaN row (zero input): np.argmax -> 0
 }
 
-__global__ void assign_full_kernel(const double* __restrict__ X, const double* __restrict__ C,
-                                   int L, int d, const int32_t* __restrict__ full_list,
-                                   const int32_t* __restrict__ n_full, int32_t* __restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); w < *n_full;
-       w += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+// A listed row is scored against every centroid by a whole block (thread =
+// centroids tid, tid + 256, ...; the row staged in shared memory), so even a
+// single listed row costs microseconds, not a warp's serial walk over L dots.
+constexpr int kFullThreads = 256;
+__global__ void __launch_bounds__(kFullThreads)
+assign_full_kernel(const double* __restrict__ X, const double* __restrict__ C, int L, int d,
+                   const int32_t* __restrict__ full_list, const int32_t* __restrict__ n_full,
+                   int32_t* __restrict__ out) {
+  extern __shared__ double xrow[];  // d
+  __shared__ double sv[kFullThreads / 32];
+  __shared__ int si[kFullThreads / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int total = *n_full;
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
     const int64_t r = full_list[w];
-    const double* x = X + r * (int64_t)d;
+    __syncthreads();
+    for (int k = threadIdx.x; k < d; k += kFullThreads) xrow[k] = X[r * (int64_t)d + k];
+    __syncthreads();
     double bv = -INFINITY;
     int bi = INT_MAX;
-    for (int l = lane; l < L; l += 32) {
-      const double e = exact_ip(x, C + (int64_t)l * d, d);
-      if (e > bv) { bv = e; bi = l; }  // ascending l per lane: lowest on ties
+    for (int l = threadIdx.x; l < L; l += kFullThreads) {
+      const double e = exact_ip(xrow, C + (int64_t)l * d, d);
+      if (e > bv) { bv = e; bi = l; }  // ascending l per thread: lowest on ties
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -544,7 +554,13 @@ __global__ void assign_full_kernel(const double* __restrict__ X, const double* _
       const int oi = __shfl_xor_sync(kFull, bi, o);
       if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
     }
-    if (lane == 0) out[r] = bi == INT_MAX ? 0 : bi;
+    if (lane == 0) { sv[warp] = bv; si[warp] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int x = 1; x < kFullThreads / 32; ++x)
+        if (sv[x] > bv || (sv[x] == bv && si[x] < bi)) { bv = sv[x]; bi = si[x]; }
+      out[r] = bi == INT_MAX ? 0 : bi;
+    }
   }
 }
 
@@ -1153,7 +1169,8 @@ static int assign_tc_t(const double* xn, const CT* centroids, int64_t n, int n_l
   assign_pick_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, prep, tv, ti, ex, list_out,
                                                                  full, nfull);
   if (int e = check_launch("assign_pick")) return e;
-  assign_full_kernel<<<148, 256, 0, s>>>(xn, c64, n_lists, dim, full, nfull, list_out);
+  assign_full_kernel<<<2 * device_sm_count(), kFullThreads, sizeof(double) * dim, s>>>(
+      xn, c64, n_lists, dim, full, nfull, list_out);
   return check_launch("assign_full");
 }
 

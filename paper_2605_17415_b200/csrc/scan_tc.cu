@@ -1025,6 +1025,46 @@ __global__ void items_fill_kernel(const int32_t* __restrict__ ntile, const int32
   for (int t = 0; t < nt; ++t) items[S[t] + atomicAdd(&fill[t], 1)] = make_int2(l, t);
 }
 
+// Item order. Tile 0 of every list first (tile 0 holds a list's nearest-rank
+// pairs: scanning those first tightens every query's global bound before its
+// far lists run), then the remaining query tiles list-major: a list's tiles
+// 1.. are consecutive items, so neighbouring CTAs stream the list at about
+// the same time and its re-reads hit L2. `first_major` = 0 makes every tile
+// list-major (measurement only). One block.
+__global__ void __launch_bounds__(1024) items_fill_listmajor_kernel(
+    const int32_t* __restrict__ ntile, int L, int first_major, int2* __restrict__ items) {
+  __shared__ int sa[1024], sb[1024];
+  const int per = (L + 1023) / 1024;
+  const int l0 = threadIdx.x * per, l1 = min(L, l0 + per);
+  int a = 0, f = 0;
+  for (int l = l0; l < l1; ++l) {
+    const int nt = ntile[l];
+    const int head = first_major && nt > 0 ? 1 : 0;
+    f += head;
+    a += nt - head;
+  }
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = f;
+  __syncthreads();
+  for (int s = 1; s < 1024; s <<= 1) {
+    const int va = threadIdx.x >= s ? sa[threadIdx.x - s] : 0;
+    const int vb = threadIdx.x >= s ? sb[threadIdx.x - s] : 0;
+    __syncthreads();
+    sa[threadIdx.x] += va;
+    sb[threadIdx.x] += vb;
+    __syncthreads();
+  }
+  const int nfirst = sb[1023];
+  a = nfirst + sa[threadIdx.x] - a;
+  f = sb[threadIdx.x] - f;
+  for (int l = l0; l < l1; ++l) {
+    const int nt = ntile[l];
+    const int head = first_major && nt > 0 ? 1 : 0;
+    if (head) items[f++] = make_int2(l, 0);
+    for (int t = head; t < nt; ++t) items[a++] = make_int2(l, t);
+  }
+}
+
 // Split each rotated query row once per search into fp16 hi/lo (scaled 2^14),
 // packed 2 per word along K, zero-padded to DP: the A-operand rows of TMEM.
 __global__ void q16_kernel(const float* __restrict__ qrot, int64_t nq, int d, int DP,
@@ -1422,7 +1462,16 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   if (int e = check_launch("tile_scan")) return e;
   pair_scatter_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.pstart2, S.cursor2, S.pairs);
   if (int e = check_launch("pair_scatter")) return e;
-  items_fill_kernel<<<(L + 255) / 256, 256, 0, s>>>(S.ntile, S.S, S.fill, L, S.items);
+  // default: tile 0 of every list first, then each list's further tiles back to
+  // back (C2 n_p=64: 211 MB of DRAM reads per scan instead of 405 MB, same
+  // time); IVFTQ_ITEMS_ORDER=tile (round 1's tile-major order) or =list
+  // (everything list-major: 114 MB, 3-12 % slower) for measurement
+  const char* order = getenv("IVFTQ_ITEMS_ORDER");
+  if (order && order[0] == 't')
+    items_fill_kernel<<<(L + 255) / 256, 256, 0, s>>>(S.ntile, S.S, S.fill, L, S.items);
+  else
+    items_fill_listmajor_kernel<<<1, 1024, 0, s>>>(S.ntile, L, order && order[0] == 'l' ? 0 : 1,
+                                                   S.items);
   if (int e = check_launch("items_fill")) return e;
 
   const int fb = st->field_bits, C = 1 << fb;
