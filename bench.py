@@ -80,7 +80,7 @@ def spawn_ranks(args) -> int:
         port = s.getsockname()[1]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
-           "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+           "--master-port", str(port), "--", str(Path(__file__).resolve())] + sys.argv[1:]
     return subprocess.call(cmd)
 
 

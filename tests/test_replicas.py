@@ -51,3 +51,27 @@ def test_single_process_defaults():
     assert world() == (0, 1)
     assert max_over_ranks(3.5, "cpu") == 3.5
     assert job_throughput(10, 2.0) == pytest.approx(5000.0)
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun relaunches itself as two ranks over
+    127.0.0.1; the reference arm (CPU oracle, rank 0 only) prints one line that
+    carries the same n_gpus as the other arm would."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run(
+        [sys.executable, str(root / "bench.py"), "--impl", "reference", "--gpus", "2", "--config",
+         "c2", "--n", "20000", "--nq", "64", "--steps", "1", "--warmup", "0",
+         "--ref-step-seconds", "0.2"],
+        capture_output=True, text=True, timeout=300, env=env, cwd=str(root))
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1                      # rank 1 exits without printing
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
