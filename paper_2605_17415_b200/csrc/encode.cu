@@ -52,6 +52,45 @@ normalize_kernel(const T* __restrict__ x, int64_t n, int d, double* __restrict__
   }
 }
 
+// Rows of 8 <= d <= 128 without shared-memory staging: eight lanes per row,
+// lane j owns numpy's pairwise accumulator r_j (elements j, j+8, ...: 64-byte
+// segments per load step, all of a lane's loads in flight at once), the three
+// xor shuffles form ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and the d % 8 tail is
+// added in order, exactly as pw_sumsq_lane8 / numpy do.
+constexpr int kDirectMax = 128;
+template <typename T>
+__global__ void __launch_bounds__(256)
+normalize_direct_kernel(const T* __restrict__ x, int64_t n, int d, double* __restrict__ xn,
+                        unsigned long long* bad) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid >> 3;
+  const int j = (int)(gid & 7);
+  const bool live = row < n;
+  const T* xr = x + (live ? row : n - 1) * (int64_t)d;
+  const int lim = d - (d % 8), cnt = lim >> 3;
+  double v[kDirectMax / 8];
+#pragma unroll
+  for (int i = 0; i < kDirectMax / 8; ++i) v[i] = i < cnt ? (double)xr[j + 8 * i] : 0.0;
+  double r = sq(v[0]);
+#pragma unroll
+  for (int i = 1; i < kDirectMax / 8; ++i)
+    if (i < cnt) r = add(r, sq(v[i]));
+  const unsigned gm = 0xffu << (threadIdx.x & 24);
+  r = add(r, __shfl_xor_sync(gm, r, 1));
+  r = add(r, __shfl_xor_sync(gm, r, 2));
+  r = add(r, __shfl_xor_sync(gm, r, 4));
+  double tail = lim + j < d ? (double)xr[lim + j] : 0.0;
+  for (int i = lim; i < d; ++i) r = add(r, sq(__shfl_sync(gm, tail, (threadIdx.x & 24) + i - lim)));
+  const double nr = __dsqrt_rn(r);
+  if (!live) return;
+  if (j == 0 && !(nr >= 1e-12) && !(nr != nr)) atomicMin(bad, (unsigned long long)row);
+  double* out = xn + row * (int64_t)d;
+#pragma unroll
+  for (int i = 0; i < kDirectMax / 8; ++i)
+    if (i < cnt) out[j + 8 * i] = __ddiv_rn(v[i], nr);
+  if (lim + j < d) out[lim + j] = __ddiv_rn(tail, nr);
+}
+
 __global__ void init_i64(int64_t* p, int64_t v) { *p = v; }
 
 __global__ void __launch_bounds__(kRowThreads)
@@ -183,6 +222,66 @@ resid_split_kernel(const double* __restrict__ xn, const float* __restrict__ cent
     split16e(k + 1 < d && q > 0.0 ? (float)(__ddiv_rn(rp[k + 1], q) * 16384.0) : 0.f, h1, l1);
     hi[(row0 + r) * hw + (k >> 1)] = h0 | ((uint32_t)h1 << 16);
     lo[(row0 + r) * hw + (k >> 1)] = l0 | ((uint32_t)l1 << 16);
+  }
+}
+
+// The same step for 8 <= d <= 128 without shared-memory staging (eight lanes
+// per row as in normalize_direct_kernel); a lane pair (j even, j + 1) packs
+// its two coordinates into one operand word.
+__global__ void __launch_bounds__(256)
+resid_split_direct_kernel(const double* __restrict__ xn, const float* __restrict__ cent,
+                          const int32_t* __restrict__ lids, int64_t n, int d, int DP, int flat,
+                          uint16_t* __restrict__ norm_out, uint32_t* __restrict__ hi,
+                          uint32_t* __restrict__ lo) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid >> 3;
+  const int j = (int)(gid & 7);
+  const bool live = row < n;
+  const int64_t rr = live ? row : n - 1;
+  const double* xr = xn + rr * (int64_t)d;
+  const float* cr = flat ? nullptr : cent + (int64_t)lids[rr] * d;
+  const int lim = d - (d % 8), cnt = lim >> 3;
+  double v[kDirectMax / 8];
+#pragma unroll
+  for (int i = 0; i < kDirectMax / 8; ++i) {
+    double t = 0.0;
+    if (i < cnt) {
+      t = xr[j + 8 * i];
+      if (cr) t = __dsub_rn(t, (double)cr[j + 8 * i]);
+    }
+    v[i] = t;
+  }
+  double tail = 0.0;
+  if (lim + j < d) {
+    tail = xr[lim + j];
+    if (cr) tail = __dsub_rn(tail, (double)cr[lim + j]);
+  }
+  double r = sq(v[0]);
+#pragma unroll
+  for (int i = 1; i < kDirectMax / 8; ++i)
+    if (i < cnt) r = add(r, sq(v[i]));
+  const unsigned gm = 0xffu << (threadIdx.x & 24);
+  r = add(r, __shfl_xor_sync(gm, r, 1));
+  r = add(r, __shfl_xor_sync(gm, r, 2));
+  r = add(r, __shfl_xor_sync(gm, r, 4));
+  for (int i = lim; i < d; ++i) r = add(r, sq(__shfl_sync(gm, tail, (threadIdx.x & 24) + i - lim)));
+  const double q = __dsqrt_rn(r);
+  if (live && j == 0) norm_out[row] = d2h_bits(q);
+  // operand words: coordinates k = j + 8 i for k < DP (zeros past d)
+  const int hw = DP / 2;
+#pragma unroll
+  for (int i = 0; i < (kDirectMax + 31) / 32 * 4; ++i) {
+    const int k = j + 8 * i;
+    if (k - j >= DP) break;  // uniform over the group
+    // k < lim: this lane's i-th element; k = lim + j < d: its tail element
+    const double val = k < lim ? v[i < kDirectMax / 8 ? i : 0] : (k < d ? tail : 0.0);
+    uint16_t h, l;
+    split16e(k < d && q > 0.0 ? (float)(__ddiv_rn(val, q) * 16384.0) : 0.f, h, l);
+    const uint32_t ph = __shfl_xor_sync(gm, (uint32_t)h, 1), pl = __shfl_xor_sync(gm, (uint32_t)l, 1);
+    if (live) {
+      if ((j & 1) == 0) hi[row * hw + (k >> 1)] = h | (ph << 16);
+      else lo[row * hw + (k >> 1)] = pl | ((uint32_t)l << 16);
+    }
   }
 }
 
@@ -460,6 +559,16 @@ extern "C" int ivftq_normalize_rows(const void* x, int x_dtype, int64_t n, int d
   init_i64<<<1, 1, 0, S(stream)>>>(bad_row, n);
   if (int e = check_launch("init_bad_row")) return e;
   if (n == 0) return 0;
+  if (dim >= 8 && dim <= kDirectMax && !getenv("IVFTQ_ROWS_STAGED")) {
+    const unsigned g = (unsigned)((n * 8 + 255) / 256);
+    if (x_dtype == IVFTQ_F32)
+      normalize_direct_kernel<float><<<g, 256, 0, S(stream)>>>((const float*)x, n, dim, xn,
+                                                                (unsigned long long*)bad_row);
+    else
+      normalize_direct_kernel<double><<<g, 256, 0, S(stream)>>>((const double*)x, n, dim, xn,
+                                                                 (unsigned long long*)bad_row);
+    return check_launch("normalize_rows");
+  }
   int grid = (int)((n + kNormRows - 1) / kNormRows);
   const size_t nsm = (size_t)kNormRows * (dim + 1) * sizeof(double);
   if (x_dtype == IVFTQ_F32) {
@@ -552,10 +661,15 @@ extern "C" int ivftq_rotate_unit_tc(const double* xn, const float* centroids,
   p += a256(ivftq_coarse_prep_bytes(dim, dim));
   uint32_t* xh = (uint32_t*)p;
   uint32_t* xl = xh + (size_t)n * (DP / 2);
-  if (int e = set_row_smem((const void*)resid_split_kernel, dim)) return e;
-  const int grid = (int)((n + kRowTile - 1) / kRowTile);
-  resid_split_kernel<<<grid, kSplitThreads, row_smem(dim), S(stream)>>>(
-      xn, centroids, list_ids, n, dim, DP, flat, norm_out, xh, xl);
+  if (dim >= 8 && dim <= kDirectMax && !getenv("IVFTQ_ROWS_STAGED")) {
+    resid_split_direct_kernel<<<(unsigned)((n * 8 + 255) / 256), 256, 0, S(stream)>>>(
+        xn, centroids, list_ids, n, dim, DP, flat, norm_out, xh, xl);
+  } else {
+    if (int e = set_row_smem((const void*)resid_split_kernel, dim)) return e;
+    const int grid = (int)((n + kRowTile - 1) / kRowTile);
+    resid_split_kernel<<<grid, kSplitThreads, row_smem(dim), S(stream)>>>(
+        xn, centroids, list_ids, n, dim, DP, flat, norm_out, xh, xl);
+  }
   if (int e = check_launch("resid_split")) return e;
   return rotate_tc(xh, xl, n, dim, R, U_out, prep, S(stream));
 }
