@@ -555,7 +555,7 @@ def test_rotate_tc_error_inside_guard(n, d, L):
     x = c[lid].astype(np.float64) + rng.standard_normal((n, d)) * rng.uniform(1e-4, 0.3, (n, 1))
     x[:3] = c[lid[:3]]                      # zero residuals
     xn = x / np.linalg.norm(x, axis=1)[:, None]
-    R = np.ascontiguousarray(generate_rotation(d, 42).matrix, dtype=np.float64)
+    R = np.array(generate_rotation(d, 42).matrix, dtype=np.float64)
     r = xn - c[lid].astype(np.float64)
     rn = np.linalg.norm(r, axis=1)
     with np.errstate(invalid="ignore", divide="ignore"):
@@ -578,6 +578,54 @@ def test_rotate_tc_error_inside_guard(n, d, L):
     err = np.abs(got[live] - want[live]).max()
     assert err < 2.0 ** -20, err
     assert np.array_equal(nrm.cpu().numpy().view(np.uint16), rn.astype(np.float16).view(np.uint16))
+
+
+@pytest.mark.parametrize("d,bits", [(96, 4), (128, 4), (64, 2), (200, 3)])
+def test_encoder_decides_near_threshold_coordinates_exactly(d, bits):
+    """Rows built so that, after rotation, a third of their coordinates sit
+    1e-9 .. 2e-6 above or below a Lloyd-Max decision threshold (bin boundary
+    or half-bin centroid): far inside the tensor-core encoder's guard, far
+    outside f64 summation noise. The guard must hand every such row to the
+    exact pass, so bins and signs equal the oracle's (index.py:256-262,
+    lloydmax.py:129-144)."""
+    from oracle import ivftq_oracle as orc
+    from paper_2605_17415_b200 import CoarsePartition, design_quantizer, generate_rotation
+    from paper_2605_17415_b200.index import IndexConfig, IvfTqIndex
+
+    rng = np.random.default_rng(100 * d + bits)
+    q = design_quantizer(bits, d)
+    R = np.asarray(generate_rotation(d, 42).matrix, dtype=np.float64)
+    thr = np.concatenate([np.asarray(q.boundaries, np.float64)[1:-1],
+                          np.asarray(q.centroids, np.float64)])
+    thr = thr[np.abs(thr) < 1.2 / np.sqrt(d)]        # inner thresholds: the row still has norm 1
+    n, m = 3000, d // 3
+    u = np.zeros((n, d))
+    for i in range(n):
+        near = rng.choice(d, m, replace=False)
+        delta = rng.choice([1e-9, 1e-8, 1e-7, 2e-6], m) * rng.choice([-1.0, 1.0], m)
+        u[i, near] = rng.choice(thr, m) + delta
+        rest = np.setdiff1d(np.arange(d), near)
+        room = 1.0 - np.sum(u[i, near] ** 2)
+        assert room > 0
+        v = rng.standard_normal(len(rest))
+        u[i, rest] = v * np.sqrt(room) / np.linalg.norm(v)
+    x = (u @ R) * rng.uniform(0.5, 2.0, (n, 1))      # rot = x~ . R^T = u up to f64 rounding
+    ph = np.zeros((1, d), np.float32)
+    ph[0, 0] = 1.0
+    idx = IvfTqIndex(IndexConfig(dim=d, bits=bits, n_lists=1, flat=True), q,
+                     generate_rotation(d, 42), CoarsePartition(1, d, ph))
+    idx.add_batch(x)
+    o = orc.OracleIndex(ph, R, q.boundaries, q.centroids, q.half_bin_means, flat=True)
+    o.add_batch(x)
+    # the construction really is adversarial for an unguarded f32 decision
+    un = x / np.linalg.norm(x, axis=1)[:, None]
+    rot = un @ R.T
+    rot /= np.linalg.norm(rot, axis=1)[:, None]
+    gap = np.abs(rot[:, :, None] - thr[None, None, :]).min(axis=2)
+    assert (gap < 3e-6).mean() > 0.25
+    assert np.array_equal(idx.bins, o.bins)
+    assert np.array_equal(idx.signs, o.signs)
+    assert np.array_equal(idx.norms.view(np.uint16), o.norms.view(np.uint16))
 
 
 def _coarse_case(seed, n, L, d, dup=True):
