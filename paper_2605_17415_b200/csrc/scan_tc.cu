@@ -944,44 +944,70 @@ __global__ void __launch_bounds__(1024) pair_scan_kernel(const int32_t* __restri
                                                          int32_t* __restrict__ ntile,
                                                          int32_t* __restrict__ G,
                                                          int32_t* __restrict__ n_items) {
-  __shared__ int sa[1024], sb[1024];
-  const int per = (L + 1023) / 1024;
-  const int l0 = threadIdx.x * per, l1 = min(L, l0 + per);
-  int a = 0, t = 0;
-  for (int l = l0; l < l1; ++l) {
-    int c = 0;
-    for (int r = 0; r < kRC; ++r) c += cnt2[l * kRC + r];
-    a += c;
-    t += (c + kM - 1) / kM;
-  }
-  sa[threadIdx.x] = a;
-  sb[threadIdx.x] = t;
+  // One list per thread, 1024 lists per pass (the class counters of a list
+  // are contiguous: coalesced loads, kept in registers for the second half),
+  // a two-level shuffle scan of (pairs, tiles) per pass with carried totals.
+  // G (per-tile-index list counts) is only needed by the tile-major item
+  // order and is skipped when null.
+  __shared__ int wa[32], wb[32];
+  __shared__ int carry_a, carry_b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) { carry_a = 0; carry_b = 0; }
   __syncthreads();
-  for (int s = 1; s < 1024; s <<= 1) {
-    int va = threadIdx.x >= s ? sa[threadIdx.x - s] : 0;
-    int vb = threadIdx.x >= s ? sb[threadIdx.x - s] : 0;
-    __syncthreads();
-    sa[threadIdx.x] += va;
-    sb[threadIdx.x] += vb;
-    __syncthreads();
-  }
-  a = sa[threadIdx.x] - a;  // exclusive
-  for (int l = l0; l < l1; ++l) {
-    pstart[l] = a;
+  for (int l0 = 0; l0 < L; l0 += 1024) {
+    const int l = l0 + threadIdx.x;
+    int cls[kRC];
     int c = 0;
+#pragma unroll
     for (int r = 0; r < kRC; ++r) {
-      pstart2[l * kRC + r] = a + c;
-      c += cnt2[l * kRC + r];
+      cls[r] = l < L ? cnt2[l * kRC + r] : 0;
+      c += cls[r];
     }
     const int nt = (c + kM - 1) / kM;
-    ntile[l] = nt;
-    for (int i = 0; i < nt; ++i) atomicAdd(&G[i], 1);
-    a += c;
+    int a = c, t = nt;  // inclusive scans
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int va = __shfl_up_sync(kFull, a, o), vb = __shfl_up_sync(kFull, t, o);
+      if (lane >= o) { a += va; t += vb; }
+    }
+    if (lane == 31) { wa[warp] = a; wb[warp] = t; }
+    __syncthreads();
+    if (warp == 0) {
+      int xa = wa[lane], xb = wb[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int va = __shfl_up_sync(kFull, xa, o), vb = __shfl_up_sync(kFull, xb, o);
+        if (lane >= o) { xa += va; xb += vb; }
+      }
+      wa[lane] = xa;
+      wb[lane] = xb;
+    }
+    __syncthreads();
+    const int base_a = carry_a + (warp ? wa[warp - 1] : 0);
+    int excl = base_a + a - c;  // exclusive pair prefix of this list
+    if (l < L) {
+      pstart[l] = excl;
+      int run = 0;
+#pragma unroll
+      for (int r = 0; r < kRC; ++r) {
+        pstart2[l * kRC + r] = excl + run;
+        run += cls[r];
+      }
+      ntile[l] = nt;
+      if (G)
+        for (int i = 0; i < nt; ++i) atomicAdd(&G[i], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 1023) {
+      carry_a += wa[31];
+      carry_b += wb[31];
+    }
+    __syncthreads();
   }
-  if (threadIdx.x == 1023) {
-    pstart[L] = sa[1023];
-    pstart2[L * kRC] = sa[1023];
-    *n_items = sb[1023];
+  if (threadIdx.x == 0) {
+    pstart[L] = carry_a;
+    pstart2[L * kRC] = carry_a;
+    *n_items = carry_b;
   }
 }
 
@@ -1456,18 +1482,22 @@ extern "C" int ivftq_scan_topk_tc(const ivftq_store* st, const int32_t* probe,
   }
   pair_count_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.cnt2);
   if (int e = check_launch("pair_count")) return e;
-  pair_scan_kernel<<<1, 1024, 0, s>>>(S.cnt2, L, S.pstart2, S.pstart, S.ntile, S.G, S.n_items);
+  const char* order = getenv("IVFTQ_ITEMS_ORDER");
+  const bool tile_major = order && order[0] == 't';
+  pair_scan_kernel<<<1, 1024, 0, s>>>(S.cnt2, L, S.pstart2, S.pstart, S.ntile,
+                                      tile_major ? S.G : nullptr, S.n_items);
   if (int e = check_launch("pair_scan")) return e;
-  tile_scan_kernel<<<1, 1024, 0, s>>>(S.G, S.T, S.S);
-  if (int e = check_launch("tile_scan")) return e;
+  if (tile_major) {
+    tile_scan_kernel<<<1, 1024, 0, s>>>(S.G, S.T, S.S);
+    if (int e = check_launch("tile_scan")) return e;
+  }
   pair_scatter_kernel<<<gp, 256, 0, s>>>(probe, np, n_p, S.pstart2, S.cursor2, S.pairs);
   if (int e = check_launch("pair_scatter")) return e;
   // default: tile 0 of every list first, then each list's further tiles back to
   // back (C2 n_p=64: 211 MB of DRAM reads per scan instead of 405 MB, same
   // time); IVFTQ_ITEMS_ORDER=tile (round 1's tile-major order) or =list
   // (everything list-major: 114 MB, 3-12 % slower) for measurement
-  const char* order = getenv("IVFTQ_ITEMS_ORDER");
-  if (order && order[0] == 't')
+  if (tile_major)
     items_fill_kernel<<<(L + 255) / 256, 256, 0, s>>>(S.ntile, S.S, S.fill, L, S.items);
   else
     items_fill_listmajor_kernel<<<1, 1024, 0, s>>>(S.ntile, L, order && order[0] == 'l' ? 0 : 1,
