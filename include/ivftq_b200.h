@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define IVFTQ_ABI_VERSION 2
+#define IVFTQ_ABI_VERSION 3  /* 3: + k-means (seed, assign_tc64, sums), tensor-core encoder tail */
 
 #define IVFTQ_OK 0
 #define IVFTQ_ERR_ARG (-1)

@@ -28,7 +28,7 @@ def test_library_exports_every_header_symbol(lib):
     for name in declared:
         assert hasattr(lib, name), name
     assert declared == set(_lib.EXPORTS), declared ^ set(_lib.EXPORTS)
-    assert lib.ivftq_abi_version() == 2
+    assert lib.ivftq_abi_version() == 3
 
 
 def test_code_layout(lib):
