@@ -303,7 +303,7 @@ __device__ __forceinline__ void vwait(uint64_t* bar, uint32_t parity, int tag) {
 // hi halves at columns dim/2 of the A buffer, lo halves DP/2 columns later.
 template <int FB, int DP, int KH>
 __device__ __forceinline__ void decode_half(const uint32_t* __restrict__ cw, int W,
-                                            const uint32_t* tab, uint32_t ta) {
+                                            uint32_t tab, uint32_t ta) {
   constexpr int FPW = 32 / FB;
   constexpr uint32_t MASK = (1u << FB) - 1u;
   constexpr int H = DP / 2, J0 = KH * H;
@@ -317,9 +317,17 @@ __device__ __forceinline__ void decode_half(const uint32_t* __restrict__ cw, int
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int j = J0 + g * 16 + 2 * e;
-      const uint32_t f0 = (wd[j / FPW - W0] >> ((j % FPW) * FB)) & MASK;
-      const uint32_t f1 = (wd[(j + 1) / FPW - W0] >> (((j + 1) % FPW) * FB)) & MASK;
-      const uint32_t t0 = tab[f0], t1 = tab[f1];
+      // field -> shared address of its table entry in a shift and one LOP3:
+      // ((w >> (s - 2)) & (MASK << 2)) | table base (the table is aligned to
+      // its size, so the OR is the add)
+      constexpr uint32_t BM = MASK << 2;
+      const int s0 = (j % FPW) * FB, s1 = ((j + 1) % FPW) * FB;
+      const uint32_t w0 = wd[j / FPW - W0], w1 = wd[(j + 1) / FPW - W0];
+      const uint32_t a0 = (((s0 >= 2) ? (w0 >> (s0 >= 2 ? s0 - 2 : 0)) : (w0 << (s0 < 2 ? 2 - s0 : 0))) & BM) | tab;
+      const uint32_t a1 = (((s1 >= 2) ? (w1 >> (s1 >= 2 ? s1 - 2 : 0)) : (w1 << (s1 < 2 ? 2 - s1 : 0))) & BM) | tab;
+      uint32_t t0, t1;
+      asm("ld.shared.u32 %0, [%1];\n" : "=r"(t0) : "r"(a0));
+      asm("ld.shared.u32 %0, [%1];\n" : "=r"(t1) : "r"(a1));
       hi[e] = __byte_perm(t0, t1, 0x5410);
       lo[e] = __byte_perm(t0, t1, 0x7632);
     }
@@ -344,7 +352,7 @@ template <int FB, int DP, int KL>
 __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
   constexpr int C = 1 << FB;
   extern __shared__ __align__(1024) unsigned char smem[];
-  __shared__ uint32_t s_tab[C];
+  __shared__ __align__(4 * C) uint32_t s_tab[C];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const Layout& Lo = P.lo;
   const int NS = P.NS, W = P.st.words_per_vec;
@@ -649,9 +657,9 @@ __global__ void __launch_bounds__(kThreads, 1) scan_vq_kernel(Params P) {
 #endif
       {
         if (kh == 0)
-          decode_half<FB, DP, 0>(cw, W, s_tab, ta);
+          decode_half<FB, DP, 0>(cw, W, sm100::smem_u32(s_tab), ta);
         else
-          decode_half<FB, DP, 1>(cw, W, s_tab, ta);
+          decode_half<FB, DP, 1>(cw, W, sm100::smem_u32(s_tab), ta);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
       sm100::tc_fence_before();
