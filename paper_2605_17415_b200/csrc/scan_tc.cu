@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
   const uint32_t tmem_cols = need <= 32 ? 32u : need <= 64 ? 64u : need <= 128 ? 128u : need <= 256 ? 256u : 512u;
   const Layout& Lo = P.lo;  // kernel-parameter space: no per-use recomputation
   // level table in static shared memory: lookups address it as reg + symbol
-  __shared__ uint32_t s_tab[C];
+  __shared__ __align__(4 * C) uint32_t s_tab[C];  // aligned to its size: base | offset == base + offset
   uint32_t* tab = s_tab;
   uint64_t* bars = (uint64_t*)(smem + Lo.bars);
   uint64_t* st_full = bars;            // [NS] producer -> decoders/epilogue (TMA tx)
@@ -716,6 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
       unsigned char* bhi = smem + (ob ? Lo.bhi[1] : Lo.bhi[0]);
       unsigned char* blo = smem + (ob ? Lo.blo[1] : Lo.blo[0]);
       const int nvshift = __ffs(NV) - 1;
+      const uint32_t tab_s = sm100::smem_u32(s_tab);
 #ifdef IVFTQ_EXP_NODEC
       if (c.nqt < 0)  // experiment build: decode skipped (timing bound only)
 #endif
@@ -736,7 +737,12 @@ __global__ void __launch_bounds__(kThreads, 1) scan_tc_kernel(Params P) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int f = cc * 8 + e;  // field within group (compile time)
-              tv[e] = s_tab[(words[f / FPW] >> ((f % FPW) * FB)) & MASK];
+              // shared address of the entry in a shift and one LOP3 (scan_vq.cu decode_half)
+              const int sh = (f % FPW) * FB;
+              const uint32_t wf = words[f / FPW];
+              const uint32_t ad = (((sh >= 2) ? (wf >> (sh >= 2 ? sh - 2 : 0)) : (wf << (sh < 2 ? 2 - sh : 0))) &
+                                   (MASK << 2)) | tab_s;
+              asm("ld.shared.u32 %0, [%1];\n" : "=r"(tv[e]) : "r"(ad));
             }
             // entry = hi | lo << 16: one byte permute packs each fp16 pair
             const uint32_t o = ch * (NV * 16) + (v >> 3) * 128 + (v & 7) * 16;
