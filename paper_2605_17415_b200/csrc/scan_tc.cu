@@ -1198,26 +1198,30 @@ seed_bound_kernel(ivftq_store st, const int32_t* __restrict__ probe,
     scw[p * 32 + lane] = v;
   }
   __syncwarp();
-  // k-th best: the largest value with at least k values >= it (slots past
-  // the list hold -inf and never qualify); candidates broadcast from shared
+  // k-th best (with multiplicity; slots past the list hold -inf): k rounds of
+  // "take the warp's maximum out", each lane holding P of the 32 P scores
   double mine[P];
-  int ge[P];
 #pragma unroll
-  for (int p = 0; p < P; ++p) {
-    mine[p] = scw[p * 32 + lane];
-    ge[p] = 0;
-  }
-  for (int o = 0; o < 32 * P; ++o) {
-    const double v = scw[o];
-#pragma unroll
-    for (int p = 0; p < P; ++p) ge[p] += v >= mine[p];
-  }
+  for (int p = 0; p < P; ++p) mine[p] = scw[p * 32 + lane];
   double kth = -INFINITY;
+  for (int it = 0; it < k; ++it) {
+    double lm = mine[0];
+    int lp = 0;
 #pragma unroll
-  for (int p = 0; p < P; ++p)
-    if (ge[p] >= k && mine[p] > -INFINITY) kth = fmax(kth, mine[p]);
+    for (int p = 1; p < P; ++p)
+      if (mine[p] > lm) { lm = mine[p]; lp = p; }
+    double gm = lm;
 #pragma unroll
-  for (int o = 16; o; o >>= 1) kth = fmax(kth, __shfl_xor_sync(kFull, kth, o));
+    for (int o = 16; o; o >>= 1) gm = fmax(gm, __shfl_xor_sync(kFull, gm, o));
+    kth = gm;
+    if (!(gm > -INFINITY)) break;  // fewer than k scores: no bound
+    const unsigned own = __ballot_sync(kFull, lm == gm);
+    if (lane == __ffs(own) - 1) {
+#pragma unroll
+      for (int p = 0; p < P; ++p)
+        if (p == lp) mine[p] = -INFINITY;
+    }
+  }
   if (lane == 0) {
     double b = -INFINITY;
     if (m >= k && kth > -INFINITY) b = kth;
