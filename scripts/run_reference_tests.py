@@ -16,7 +16,9 @@ Two steps, both test infrastructure (nothing here is on the product path):
       .rotation, .lloydmax -> our modules; ivftq.data_io -> the staged
       reference generator) and run the staged tests with pytest.
 
-The log of the last GPU run is committed as profiles/r2_reference_tests.log;
+The staged copy is scratch: it is removed again after the run (`rm -rf baseline`),
+so the working tree never keeps reference files. The log of the last GPU run
+is committed as profiles/r2_reference_tests.log;
 every failure/exclusion is listed with its reason in DESIGN.md (c).
 """
 
